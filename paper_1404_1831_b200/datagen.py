@@ -1,0 +1,72 @@
+"""Seeded synthetic workloads named by BASELINE.json.
+
+The paper's BIGANN/GIST sets are not available; these
+generators stand in with the configs' shapes and value distributions.
+
+* ``clipped_mixture`` -- configs 0/1/2/4: ``x = clip(round(c_j + 20 z), 0, 255)``
+  with ``j ~ U{0..ncomp-1}``, ``c_j ~ U[0,100]^D``, ``z ~ N(0, I)``.  Centres
+  come from seed 0, the database from seed 1, queries from seed 2 and the
+  training draw from seed 3 (BASELINE.json configs[0]).
+* ``normalized_mixture`` -- config 3: centres ``N(0, I)``, within-component
+  sigma 0.3, then L2-normalised.
+
+The numpy versions are the reference-side generators (used to export the
+config-0 index from the reference); the torch versions draw the same
+distributions on the GPU for the 10M-1B point configs, where a host draw
+would dominate setup time.  They are not bit-identical streams.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+SEED_CENTRES, SEED_BASE, SEED_QUERIES, SEED_TRAIN = 0, 1, 2, 3
+
+
+def mixture_centres(ncomp: int, dim: int, seed: int = SEED_CENTRES) -> np.ndarray:
+    return np.random.default_rng(seed).uniform(0.0, 100.0, (ncomp, dim))
+
+
+def clipped_mixture(n: int, dim: int, ncomp: int, seed: int, centres=None) -> np.ndarray:
+    """numpy draw: component indices first, then the normals."""
+    if centres is None:
+        centres = mixture_centres(ncomp, dim)
+    rng = np.random.default_rng(seed)
+    j = rng.integers(0, ncomp, n)
+    z = rng.standard_normal((n, dim))
+    return np.clip(np.round(centres[j] + 20.0 * z), 0, 255).astype(np.float32)
+
+
+def clipped_mixture_torch(n: int, dim: int, ncomp: int, seed: int, device, centres=None, chunk=1 << 22):
+    """Same distribution drawn on ``device`` with a seeded torch generator."""
+    import torch
+
+    if centres is None:
+        centres = mixture_centres(ncomp, dim)
+    cent = torch.as_tensor(centres, dtype=torch.float32, device=device)
+    g = torch.Generator(device=device)
+    g.manual_seed(1_000_003 * seed + 17)
+    out = torch.empty((n, dim), dtype=torch.float32, device=device)
+    for s in range(0, n, chunk):
+        e = min(n, s + chunk)
+        j = torch.randint(0, ncomp, (e - s,), generator=g, device=device)
+        z = torch.randn((e - s, dim), generator=g, device=device)
+        out[s:e] = torch.clamp(torch.round(cent[j] + 20.0 * z), 0, 255)
+    return out
+
+
+def normalized_mixture_torch(n: int, dim: int, ncomp: int, seed: int, device, sigma=0.3, chunk=1 << 22):
+    import torch
+
+    gc = torch.Generator(device=device)
+    gc.manual_seed(SEED_CENTRES + 7)
+    cent = torch.randn((ncomp, dim), generator=gc, device=device)
+    g = torch.Generator(device=device)
+    g.manual_seed(1_000_003 * seed + 29)
+    out = torch.empty((n, dim), dtype=torch.float32, device=device)
+    for s in range(0, n, chunk):
+        e = min(n, s + chunk)
+        j = torch.randint(0, ncomp, (e - s,), generator=g, device=device)
+        x = cent[j] + sigma * torch.randn((e - s, dim), generator=g, device=device)
+        out[s:e] = x / torch.linalg.vector_norm(x, dim=1, keepdim=True)
+    return out
