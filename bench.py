@@ -1,0 +1,374 @@
+"""Benchmark: batched bilayer-PQ search on B200 (BASELINE.json metric).
+
+Metric: queries/s at fixed L, k (plus PQ codes scanned/s and the fused
+traversal+scan kernel's HBM roofline fraction).  Default workload is
+BASELINE.json configs[1] (single-GPU FBPQ): N=10M clipped-integer mixture
+vectors (D=128, 4,096 components), T=4,096 per half, M=8 x 256, 10,000
+queries, L=10,000, k=100.  Data is seeded synthetic (the paper's BIGANN is
+not available); codebooks are trained on the device (setup, untimed).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config c1|c0|c2] [--engine fbpq|baseline|hbpq] [--L ..] [--k ..]
+
+N>1 (torchrun): replicas -- every rank builds the same index and searches its
+own 10k-query batch (weak scaling; c1 fits one GPU); value is
+the whole-job rate over the max-over-ranks device time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PEAKS = {}
+try:
+    PEAKS = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+except Exception:
+    pass
+HBM_PEAK = float(PEAKS.get("hbm_gbs", 6650.0))
+HBM_PEAK_SRC = "measured" if "hbm_gbs" in PEAKS else "fallback"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# --------------------------------------------------------------------- setup
+CONFIGS = {
+    "c1": dict(n=10_000_000, dim=128, ncomp=4096, t=4096, m=8, k=256, nq=10_000, L=10_000, topk=100,
+               engine="fbpq", train=262_144),
+    "c2": dict(n=10_000_000, dim=128, ncomp=4096, t=4096, m=8, k=256, nq=10_000, L=10_000, topk=100,
+               engine="hbpq", train=262_144),
+    "c1small": dict(n=1_000_000, dim=128, ncomp=4096, t=1024, m=8, k=256, nq=10_000, L=10_000, topk=100,
+                    engine="fbpq", train=131_072),
+}
+
+
+def build_workload(cfg, device, rank=0):
+    """Returns (DeviceIndex, queries [nq, D] device f32, host arrays for the CPU baseline)."""
+    import torch
+
+    from paper_1404_1831_b200 import datagen, encode
+
+    name = cfg["name"]
+    if name == "c0":
+        g = np.load(ROOT / "tests" / "golden" / "c0.npz")
+        from paper_1404_1831_b200 import DeviceIndex
+
+        tables = (g["cn1"], g["cn2"], g["fine_norms"], g["cross1"], g["cross2"])
+        dix = DeviceIndex(c1=g["c1"], c2=g["c2"], offsets=g["offsets"], ids=g["ids"], codes=g["codes"],
+                          books=g["books"], tables=tables, device=device)
+        q = torch.from_numpy(g["queries"].astype(np.float32)).to(device)
+        host = dict(c1=g["c1"], c2=g["c2"], offsets=g["offsets"], ids=g["ids"], codes=g["codes"], books=g["books"],
+                    tables=tables)
+        return dix, q, host
+    t0 = time.time()
+    cent = datagen.mixture_centres(cfg["ncomp"], cfg["dim"])
+    train = datagen.clipped_mixture_torch(cfg["train"], cfg["dim"], cfg["ncomp"], datagen.SEED_TRAIN, device, cent)
+    dh = cfg["dim"] // 2
+    c1 = encode.train_kmeans(train[:, :dh].contiguous(), cfg["t"], iters=8, seed=11)
+    c2 = encode.train_kmeans(train[:, dh:].contiguous(), cfg["t"], iters=8, seed=12)
+    i_idx, j_idx = encode.assign_cells(train, c1, c2)
+    c1t = torch.from_numpy(c1).to(device)
+    c2t = torch.from_numpy(c2).to(device)
+    disp = train - torch.cat([c1t[i_idx], c2t[j_idx]], 1)
+    ds = cfg["dim"] // cfg["m"]
+    books = np.stack([encode.train_kmeans(disp[:, p * ds:(p + 1) * ds].contiguous(), cfg["k"], iters=8, seed=20 + p)
+                      for p in range(cfg["m"])])
+    log(f"[setup] codebooks trained in {time.time() - t0:.1f}s")
+    base = datagen.clipped_mixture_torch(cfg["n"], cfg["dim"], cfg["ncomp"], datagen.SEED_BASE, device, cent)
+    if cfg["engine"] == "hbpq":
+        # local books per half-codeword: pooled residual books + per-row perturbation
+        # (bank training is out of scope; codes are encoded against these books)
+        m2 = cfg["m"] // 2
+        gen = torch.Generator(device=device)
+        gen.manual_seed(5)
+        b = torch.from_numpy(books).to(device)
+        bank1 = (b[None, :m2] + 0.5 * torch.randn((cfg["t"], m2) + b.shape[1:], generator=gen, device=device)).cpu().numpy()
+        bank2 = (b[None, m2:] + 0.5 * torch.randn((cfg["t"], m2) + b.shape[1:], generator=gen, device=device)).cpu().numpy()
+        dix = encode.build_hbpq_index(base, c1, c2, bank1, bank2, device=device)
+        host_books = dict(bank1=bank1, bank2=bank2)
+    else:
+        dix = encode.build_index(base, c1, c2, books, device=device)
+        host_books = dict(books=books)
+    del base
+    torch.cuda.empty_cache()
+    q = datagen.clipped_mixture_torch(cfg["nq"], cfg["dim"], cfg["ncomp"], datagen.SEED_QUERIES + 1000 * rank,
+                                      device, cent)
+    log(f"[setup] index built in {time.time() - t0:.1f}s: N={dix.n} populated="
+        f"{int((torch.diff(dix.offsets.long() & 0xFFFFFFFF) > 0).sum())}")
+    host = dict(c1=c1, c2=c2, offsets=(dix.offsets.cpu().numpy().view(np.uint32)).astype(np.int64),
+                ids=dix.ids.cpu().numpy().view(np.uint32), codes=dix.codes.cpu().numpy(), **host_books)
+    if cfg["engine"] != "hbpq":
+        host["tables"] = (dix.cn1.cpu().numpy(), dix.cn2.cpu().numpy(), dix.fine_norms.cpu().numpy(),
+                          dix.cross1.cpu().numpy(), dix.cross2.cpu().numpy())
+    return dix, q, host
+
+
+# -------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------- CPU baseline
+def cpu_search(host, engine, queries, L, k, threads):
+    from oracle import oracle as orc
+
+    idx = orc.Index(host["c1"], host["c2"], host["offsets"], host["ids"], host["codes"], books=host.get("books"),
+                    bank1=host.get("bank1"), bank2=host.get("bank2"), tables=host.get("tables"))
+    t0 = time.perf_counter()
+    d, i, c, nc = orc.search_batch_c(idx, engine, queries, L, k, threads=threads)
+    return time.perf_counter() - t0, nc
+
+
+def cpu_baseline(host, engine, queries_np, L, k, budget_s=20.0):
+    threads = os.cpu_count() or 1
+    # calibrate on a small sample, then size the sample to ~budget_s
+    n0 = min(len(queries_np), max(threads, 16))
+    dt, _ = cpu_search(host, engine, queries_np[:n0], L, k, threads)
+    per_q = dt / n0
+    n = int(min(len(queries_np), max(n0, budget_s / max(per_q, 1e-6))))
+    dt, nc = cpu_search(host, engine, queries_np[:n], L, k, threads)
+    return {"value": n / dt, "unit": "queries/s", "cores": threads, "kind": "port",
+            "sample": f"first {n} of {len(queries_np)} queries, same index, L={L}, k={k}, "
+                      f"C oracle (oracle/bpq_oracle.c) with {threads} POSIX threads",
+            "codes_per_s": float(nc.sum()) / dt}
+
+
+# ------------------------------------------------------------------------ run
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c1")
+    ap.add_argument("--engine", default=None)
+    ap.add_argument("--L", type=int, default=None)
+    ap.add_argument("--k", type=int, default=None)
+    ap.add_argument("--nq", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference" and rank != 0:
+        return
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    device = torch.device("cuda", local_rank)
+
+    if args.config == "c0":
+        cfg = dict(name="c0", nq=1000, L=10_000, topk=100, engine="fbpq", m=8, t=64, n=100_000, dim=128)
+    else:
+        cfg = dict(CONFIGS[args.config], name=args.config)
+    if args.engine:
+        cfg["engine"] = args.engine
+    if args.L:
+        cfg["L"] = args.L
+    if args.k:
+        cfg["topk"] = args.k
+    if args.nq:
+        cfg["nq"] = args.nq
+    engine, L, k = cfg["engine"], cfg["L"], cfg["topk"]
+    dix, q, host = build_workload(cfg, device, rank)
+    nq = q.shape[0]
+    workload = (f"{cfg['name']}: {engine} N={dix.n:,} D={dix.dim} T={dix.t} M={dix.m}x{dix.k} "
+                f"nq={nq} L={L} k={k}")
+    config = {"workload": workload, "engine": engine, "N": dix.n, "D": dix.dim, "T": dix.t, "M": dix.m,
+              "nq": nq, "L": L, "k": k, "parallelism": f"replicas{args.gpus}" if world > 1 else "single",
+              "l2": "flushed between timed steps (256 MiB write)"}
+    metric = "queries/s (batched search at fixed L, k)"
+
+    if args.impl == "reference":
+        qn = q.cpu().numpy()
+        steps_v = []
+        for s in range(args.warmup + args.steps):
+            per = max(1, 64 // 1)
+            lo = (s * per) % max(1, nq - per)
+            dt, nc = cpu_search(host, engine, qn[lo:lo + per], L, k, os.cpu_count())
+            if s >= args.warmup:
+                steps_v.append((per, dt, float(nc.sum())))
+        tot_q = sum(x[0] for x in steps_v)
+        tot_t = sum(x[1] for x in steps_v)
+        v = tot_q / tot_t
+        line = {"impl": "reference", "metric": metric, "value": v, "unit": "queries/s", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": config,
+                "cpu_baseline": {"value": v, "unit": "queries/s", "cores": os.cpu_count(), "kind": "port",
+                                 "sample": f"{steps_v[0][0]} queries per step (of {nq}), C port of the reference "
+                                           f"search (oracle/bpq_oracle.c), {os.cpu_count()} threads"},
+                "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                "codes_per_s": sum(x[2] for x in steps_v) / tot_t}
+        print(json.dumps(line), flush=True)
+        return
+
+    from paper_1404_1831_b200.index import SearchResult
+
+    ws = dix.make_workspace(engine, nq, L, k)
+    out = SearchResult(torch.empty((nq, k), dtype=torch.float32, device=device),
+                       torch.empty((nq, k), dtype=torch.int32, device=device),
+                       torch.empty((nq,), dtype=torch.int32, device=device),
+                       torch.empty((nq,), dtype=torch.int64, device=device))
+    popped = torch.empty((nq,), dtype=torch.int64, device=device)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+    stream = torch.cuda.current_stream()
+
+    # one untimed pass for the work counts (candidates and popped cells)
+    dix.search(q, L, k, engine, out=out, workspace=ws, ncand=True, popped=popped)
+    torch.cuda.synchronize()
+    counts = out.counts.cpu().numpy()
+    if (counts < 0).any():
+        raise RuntimeError(f"{int((counts < 0).sum())} queries hit the tie-plateau limit")
+    ncand = int(out.ncand.sum().item())
+    npop = int(popped.sum().item())
+    for _ in range(args.warmup):
+        dix.search(q, L, k, engine, out=out, workspace=ws)
+    torch.cuda.synchronize()
+
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        for s in range(args.steps):
+            flush.fill_(s & 0xFF)  # L2 flush, outside the event pair
+            dix.search(q, L, k, engine, out=out, workspace=ws, stage_events=evs[s])
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms = [evs[s][0].elapsed_time(evs[s][3]) for s in range(args.steps)]
+    stage_ms = np.array([[evs[s][i].elapsed_time(evs[s][i + 1]) for i in range(3)] for s in range(args.steps)])
+    t_ms = float(np.sum(step_ms))
+    if world > 1:
+        tt = torch.tensor([t_ms], device=device)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+    value = world * nq * args.steps / (t_ms / 1e3)
+
+    # end to end through the public API with host buffers
+    q_host = q.cpu().pin_memory()
+    od_h = torch.empty((nq, k), dtype=torch.float32).pin_memory()
+    oi_h = torch.empty((nq, k), dtype=torch.int32).pin_memory()
+    oc_h = torch.empty((nq,), dtype=torch.int32).pin_memory()
+    q_dev = torch.empty_like(q)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2e_ms = 0.0
+    for s in range(args.steps):
+        flush.fill_((s + 7) & 0xFF)
+        e0.record(stream)
+        q_dev.copy_(q_host, non_blocking=True)
+        dix.search(q_dev, L, k, engine, out=out, workspace=ws)
+        od_h.copy_(out.dists, non_blocking=True)
+        oi_h.copy_(out.ids, non_blocking=True)
+        oc_h.copy_(out.counts, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms += e0.elapsed_time(e1)
+    e2e_v = world * nq * args.steps / (e2e_ms / 1e3)
+
+    # roofline of the fused traversal+scan kernel ((M+4) B per candidate + 16 B per popped cell)
+    search_ms = float(np.mean(stage_ms[:, 2]))
+    alg_bytes = (dix.m + 4) * ncand + 16 * npop
+    achieved = alg_bytes / (search_ms / 1e3) / 1e9
+    line = {
+        "metric": metric, "value": value, "unit": "queries/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded BASELINE.json generator)",
+        "config": config,
+        "codes_scanned_per_s": world * ncand * args.steps / (t_ms / 1e3),
+        "stage_ms": {"first_layer": float(np.mean(stage_ms[:, 0])), "row_sort": float(np.mean(stage_ms[:, 1])),
+                     "traverse_scan_topk": search_ms},
+        "work_per_step": {"candidates": ncand, "popped_cells": npop, "cand_per_query": ncand / nq},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": HBM_PEAK, "unit": "GB/s",
+                     "frac": achieved / HBM_PEAK, "traffic": None,
+                     "kernel": "search_kernel (fused traversal + scan + top-k)",
+                     "peak_source": HBM_PEAK_SRC, "alg_bytes_per_launch": alg_bytes},
+        "e2e": {"value": e2e_v, "unit": "queries/s", "h2d_bytes_per_step": int(q.numel() * 4),
+                "d2h_bytes_per_step": int(nq * k * 8 + nq * 4)},
+        "gpu_launches": 3 * args.steps,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline(host, engine, q.cpu().numpy(), L, k)
+        except Exception as e:  # the baseline is reported, never required
+            line["cpu_baseline"] = {"error": repr(e)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,83 @@
+// Internal definitions shared by the engine's translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "bpq_b200.h"
+
+namespace bpq {
+
+void set_error(const std::string &msg);
+int fail(int code, const std::string &msg);
+
+#define BPQ_CUDA_TRY(expr)                                                                   \
+    do {                                                                                     \
+        cudaError_t _e = (expr);                                                             \
+        if (_e != cudaSuccess)                                                               \
+            return ::bpq::fail(BPQ_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+#define BPQ_CHECK(cond, code, msg)                                                           \
+    do {                                                                                     \
+        if (!(cond)) return ::bpq::fail((code), (msg));                                      \
+    } while (0)
+
+// Tunables of the fused traversal + scan + top-k kernel.
+constexpr int kSearchThreads = 256;     // threads per CTA (one CTA per query at a time)
+constexpr int kTopkBuf = 2048;          // per-CTA top-k candidate buffer (u64 keys)
+constexpr int kMaxK = kTopkBuf - kSearchThreads;  // largest k the engine accepts
+constexpr int kSortCap = 1024;          // final-band cells sorted in shared memory
+constexpr int kBandCap = 32768;         // max cells enumerated per band
+constexpr int kMaxDim = 1024;           // queries staged in shared memory
+
+struct Index {
+    int32_t D, T, M, K, dh, ds;
+    int64_t N;
+    int64_t N_global;
+    const float *c1, *c2, *cn1, *cn2;
+    const uint32_t *loff, *goff;
+    const uint32_t *ids;
+    const uint8_t *codes;
+    const float *books, *fine_norms, *cross1, *cross2, *bank1, *bank2;
+    std::vector<void *> owned;
+};
+
+// ---- launchers implemented in the .cu files --------------------------------
+int launch_coarse_dots(const float *queries, int64_t nq, int32_t D, const float *c1,
+                       const float *c2, int32_t T, float *dots1, float *dots2,
+                       cudaStream_t stream);
+int launch_row_sort(const float *queries, int64_t nq, int32_t D, const float *dots1,
+                    const float *dots2, const float *cn1, const float *cn2, int32_t T,
+                    float *sr1, float *sr2, int32_t *ord1, int32_t *ord2, cudaStream_t stream);
+
+struct SearchWorkspace {
+    float *dots1, *dots2, *sr1, *sr2;
+    int32_t *ord1, *ord2;
+    unsigned int *counter;
+    char *cta_scratch;
+    size_t cta_stride;
+    int n_cta;
+};
+
+size_t search_cta_scratch_bytes(int32_t T);
+int search_grid_ctas(int engine, int M);
+int launch_search(const Index &ix, int engine, const float *queries, int64_t q0, int64_t nq,
+                  int64_t budget, int32_t k, const SearchWorkspace &ws, float *out_dist,
+                  uint32_t *out_ids, int32_t *out_count, int64_t *out_ncand,
+                  int64_t *out_popped, cudaStream_t stream);
+int launch_traverse_stage(const double *sr1, const double *sr2, const int32_t *o1,
+                          const int32_t *o2, const int64_t *offsets, int64_t t, int64_t budget,
+                          int64_t total, int32_t *vis_i, int32_t *vis_j, int64_t *starts,
+                          int64_t *ends, int64_t *nvis_out, void *ws, size_t ws_bytes,
+                          cudaStream_t stream);
+size_t traverse_stage_ws_bytes(int64_t t, int64_t budget, int64_t total);
+
+}  // namespace bpq
+
+struct bpq_index {
+    bpq::Index ix;
+};

@@ -1,0 +1,268 @@
+// C ABI: index lifecycle, batched search orchestration, traversal stage.
+#include <algorithm>
+#include <cstring>
+#include <string>
+
+#include "bpq_internal.cuh"
+
+namespace bpq {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+
+int fail(int code, const std::string &msg) {
+    set_error(msg);
+    return code;
+}
+
+namespace {
+
+size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct SearchLayout {
+    int64_t chunk;
+    size_t dots1, dots2, sr1, sr2, ord1, ord2, counter, cta, cta_stride, total;
+    int n_cta;
+};
+
+int64_t query_chunk(int64_t nq, int32_t T) {
+    // keep the per-chunk first-layer buffers (6 arrays of [chunk, T] x 4 B) near 2 GiB
+    int64_t per_q = (int64_t)T * 24;
+    int64_t c = ((int64_t)2 << 30) / per_q;
+    c = std::max<int64_t>(c, 256);
+    return std::max<int64_t>(1, std::min<int64_t>(nq, c));
+}
+
+bool layout_for(const Index &ix, int64_t nq, SearchLayout *L) {
+    SearchLayout s{};
+    s.chunk = query_chunk(nq, ix.T);
+    int n_cta = search_grid_ctas(BPQ_ENGINE_FBPQ, ix.M);
+    if (n_cta <= 0) return false;
+    s.n_cta = n_cta;
+    size_t row = (size_t)s.chunk * ix.T * 4;
+    size_t o = 0;
+    s.dots1 = o; o += al(row);
+    s.dots2 = o; o += al(row);
+    s.sr1 = o; o += al(row);
+    s.sr2 = o; o += al(row);
+    s.ord1 = o; o += al(row);
+    s.ord2 = o; o += al(row);
+    s.counter = o; o += al(4);
+    s.cta_stride = al(search_cta_scratch_bytes(ix.T));
+    s.cta = o; o += s.cta_stride * n_cta;
+    s.total = o;
+    *L = s;
+    return true;
+}
+
+template <typename T>
+int copy_in(const T *host, size_t count, std::vector<void *> &owned, const T **dst) {
+    if (host == nullptr) {
+        *dst = nullptr;
+        return BPQ_OK;
+    }
+    void *p = nullptr;
+    BPQ_CUDA_TRY(cudaMalloc(&p, std::max<size_t>(count * sizeof(T), 1)));
+    owned.push_back(p);
+    BPQ_CUDA_TRY(cudaMemcpy(p, host, count * sizeof(T), cudaMemcpyHostToDevice));
+    *dst = static_cast<const T *>(p);
+    return BPQ_OK;
+}
+
+}  // namespace
+}  // namespace bpq
+
+using namespace bpq;
+
+extern "C" const char *bpq_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" int bpq_abi_version(void) { return BPQ_ABI_VERSION; }
+
+extern "C" int bpq_index_create(const bpq_index_desc *d, int copy_from_host, bpq_index **out) {
+    BPQ_CHECK(d != nullptr && out != nullptr, BPQ_ERR_INVALID, "null descriptor");
+    // parameter rules of multi_index._check_fine_params (multi_index.py:199-207)
+    BPQ_CHECK(d->num_parts >= 2 && d->num_parts % 2 == 0, BPQ_ERR_INVALID,
+              "number of parts must be even and >= 2");
+    BPQ_CHECK(d->num_parts <= 16, BPQ_ERR_INVALID, "number of parts must be <= 16");
+    BPQ_CHECK(d->dim > 0 && d->dim % d->num_parts == 0 && d->dim % 2 == 0, BPQ_ERR_INVALID,
+              "dimension is not divisible into parts");
+    BPQ_CHECK(d->codebook_size >= 1 && d->codebook_size <= 256, BPQ_ERR_INVALID,
+              "codebook size must be in [1, 256]");
+    BPQ_CHECK(d->num_coarse >= 1 && d->num_coarse < 65536, BPQ_ERR_UNSUPPORTED,
+              "num_coarse must be in [1, 65535]");
+    BPQ_CHECK(d->num_coarse <= 16384, BPQ_ERR_UNSUPPORTED,
+              "num_coarse > 16384 exceeds the row-sort kernel");
+    BPQ_CHECK(d->dim <= kMaxDim, BPQ_ERR_UNSUPPORTED, "dim > 1024 exceeds the search kernel");
+    BPQ_CHECK(d->num_entries >= 0 && d->num_entries <= 0xFFFFFFFFll, BPQ_ERR_UNSUPPORTED,
+              "entries must fit uint32 offsets");
+    BPQ_CHECK(d->num_entries_global >= d->num_entries && d->num_entries_global <= 0xFFFFFFFFll,
+              BPQ_ERR_INVALID, "global entry count must be >= local and fit uint32");
+    BPQ_CHECK(d->coarse1 && d->coarse2 && d->coarse_norms1 && d->coarse_norms2 && d->cell_offsets &&
+                  d->ids && d->codes,
+              BPQ_ERR_INVALID, "coarse books, norms, offsets, ids and codes are required");
+    bpq_index *h = new bpq_index();
+    Index &ix = h->ix;
+    ix.D = d->dim;
+    ix.T = d->num_coarse;
+    ix.M = d->num_parts;
+    ix.K = d->codebook_size;
+    ix.dh = d->dim / 2;
+    ix.ds = d->dim / d->num_parts;
+    ix.N = d->num_entries;
+    ix.N_global = d->num_entries_global;
+    const size_t T = ix.T, D = ix.D, M = ix.M, K = ix.K, N = ix.N, dh = ix.dh, ds = ix.ds;
+    if (!copy_from_host) {
+        ix.c1 = d->coarse1;
+        ix.c2 = d->coarse2;
+        ix.cn1 = d->coarse_norms1;
+        ix.cn2 = d->coarse_norms2;
+        ix.loff = d->cell_offsets;
+        ix.goff = d->global_offsets ? d->global_offsets : d->cell_offsets;
+        ix.ids = d->ids;
+        ix.codes = d->codes;
+        ix.books = d->fine_books;
+        ix.fine_norms = d->fine_norms;
+        ix.cross1 = d->cross1;
+        ix.cross2 = d->cross2;
+        ix.bank1 = d->bank1;
+        ix.bank2 = d->bank2;
+    } else {
+        int rc = 0;
+        rc |= copy_in(d->coarse1, T * dh, ix.owned, &ix.c1);
+        rc |= copy_in(d->coarse2, T * dh, ix.owned, &ix.c2);
+        rc |= copy_in(d->coarse_norms1, T, ix.owned, &ix.cn1);
+        rc |= copy_in(d->coarse_norms2, T, ix.owned, &ix.cn2);
+        rc |= copy_in(d->cell_offsets, T * T + 1, ix.owned, &ix.loff);
+        if (d->global_offsets)
+            rc |= copy_in(d->global_offsets, T * T + 1, ix.owned, &ix.goff);
+        else
+            ix.goff = ix.loff;
+        rc |= copy_in(d->ids, N, ix.owned, &ix.ids);
+        rc |= copy_in(d->codes, N * M, ix.owned, &ix.codes);
+        rc |= copy_in(d->fine_books, M * K * ds, ix.owned, &ix.books);
+        rc |= copy_in(d->fine_norms, M * K, ix.owned, &ix.fine_norms);
+        rc |= copy_in(d->cross1, T * (M / 2) * K, ix.owned, &ix.cross1);
+        rc |= copy_in(d->cross2, T * (M / 2) * K, ix.owned, &ix.cross2);
+        rc |= copy_in(d->bank1, T * (M / 2) * K * ds, ix.owned, &ix.bank1);
+        rc |= copy_in(d->bank2, T * (M / 2) * K * ds, ix.owned, &ix.bank2);
+        (void)D;
+        if (rc) {
+            std::string msg = g_last_error;
+            bpq_index_destroy(h);
+            return fail(BPQ_ERR_CUDA, msg);
+        }
+    }
+    *out = h;
+    return BPQ_OK;
+}
+
+extern "C" int bpq_index_destroy(bpq_index *index) {
+    if (!index) return BPQ_OK;
+    for (void *p : index->ix.owned) cudaFree(p);
+    delete index;
+    return BPQ_OK;
+}
+
+extern "C" size_t bpq_search_workspace_size(const bpq_index *index, int engine, int64_t nq,
+                                            int64_t budget, int32_t k) {
+    (void)engine;
+    (void)budget;
+    (void)k;
+    if (!index) return 0;
+    SearchLayout L;
+    if (!layout_for(index->ix, std::max<int64_t>(nq, 1), &L)) return 0;
+    return L.total;
+}
+
+extern "C" int bpq_search(const bpq_index *index, int engine, const float *queries, int64_t nq,
+                          int64_t budget, int32_t k, float *out_dist, uint32_t *out_ids,
+                          int32_t *out_count, int64_t *out_ncand, void *workspace,
+                          size_t workspace_bytes, void *stream) {
+    return bpq_search_ex(index, engine, queries, nq, budget, k, out_dist, out_ids, out_count,
+                         out_ncand, nullptr, nullptr, workspace, workspace_bytes, stream);
+}
+
+extern "C" int bpq_search_ex(const bpq_index *index, int engine, const float *queries, int64_t nq,
+                             int64_t budget, int32_t k, float *out_dist, uint32_t *out_ids,
+                             int32_t *out_count, int64_t *out_ncand, int64_t *out_popped,
+                             void *const *stage_events, void *workspace, size_t workspace_bytes,
+                             void *stream) {
+    BPQ_CHECK(index != nullptr, BPQ_ERR_INVALID, "null index");
+    const Index &ix = index->ix;
+    // traverse() rejects budget < 1 (multi_index.py:308-309); search_* reject r < 1
+    BPQ_CHECK(budget >= 1, BPQ_ERR_INVALID, "budget must be >= 1");
+    BPQ_CHECK(k >= 1, BPQ_ERR_INVALID, "r must be >= 1");
+    BPQ_CHECK(k <= kMaxK, BPQ_ERR_UNSUPPORTED, "k exceeds the engine's top-k buffer (1792)");
+    BPQ_CHECK(nq >= 0, BPQ_ERR_INVALID, "nq must be >= 0");
+    switch (engine) {
+        case BPQ_ENGINE_BASELINE:
+            BPQ_CHECK(ix.books, BPQ_ERR_INVALID, "engine baseline requires global fine codebooks");
+            break;
+        case BPQ_ENGINE_FBPQ:
+            BPQ_CHECK(ix.books && ix.fine_norms && ix.cross1 && ix.cross2, BPQ_ERR_INVALID,
+                      "engine fbpq requires fine codebooks and FBPQ tables");
+            break;
+        case BPQ_ENGINE_HBPQ:
+            BPQ_CHECK(ix.bank1 && ix.bank2, BPQ_ERR_INVALID,
+                      "engine hbpq requires an index built with local codebooks");
+            break;
+        default:
+            return fail(BPQ_ERR_INVALID, "unknown engine");
+    }
+    if (nq == 0) return BPQ_OK;
+    SearchLayout L;
+    BPQ_CHECK(layout_for(ix, nq, &L), BPQ_ERR_CUDA, "cannot size the search grid");
+    BPQ_CHECK(workspace != nullptr && workspace_bytes >= L.total, BPQ_ERR_WORKSPACE,
+              "search workspace too small (see bpq_search_workspace_size)");
+    char *w = static_cast<char *>(workspace);
+    SearchWorkspace ws{};
+    ws.dots1 = reinterpret_cast<float *>(w + L.dots1);
+    ws.dots2 = reinterpret_cast<float *>(w + L.dots2);
+    ws.sr1 = reinterpret_cast<float *>(w + L.sr1);
+    ws.sr2 = reinterpret_cast<float *>(w + L.sr2);
+    ws.ord1 = reinterpret_cast<int32_t *>(w + L.ord1);
+    ws.ord2 = reinterpret_cast<int32_t *>(w + L.ord2);
+    ws.counter = reinterpret_cast<unsigned int *>(w + L.counter);
+    ws.cta_scratch = w + L.cta;
+    ws.cta_stride = L.cta_stride;
+    ws.n_cta = L.n_cta;
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool ev = stage_events != nullptr && L.chunk >= nq;
+    if (ev) BPQ_CUDA_TRY(cudaEventRecord((cudaEvent_t)stage_events[0], s));
+    for (int64_t q0 = 0; q0 < nq; q0 += L.chunk) {
+        int64_t n = std::min<int64_t>(L.chunk, nq - q0);
+        const float *qc = queries + q0 * ix.D;
+        int rc = launch_coarse_dots(qc, n, ix.D, ix.c1, ix.c2, ix.T, ws.dots1, ws.dots2, s);
+        if (rc) return rc;
+        if (ev) BPQ_CUDA_TRY(cudaEventRecord((cudaEvent_t)stage_events[1], s));
+        rc = launch_row_sort(qc, n, ix.D, ws.dots1, ws.dots2, ix.cn1, ix.cn2, ix.T, ws.sr1, ws.sr2,
+                             ws.ord1, ws.ord2, s);
+        if (rc) return rc;
+        if (ev) BPQ_CUDA_TRY(cudaEventRecord((cudaEvent_t)stage_events[2], s));
+        rc = launch_search(ix, engine, qc, q0, n, budget, k, ws, out_dist, out_ids, out_count,
+                           out_ncand, out_popped, s);
+        if (rc) return rc;
+        if (ev) BPQ_CUDA_TRY(cudaEventRecord((cudaEvent_t)stage_events[3], s));
+    }
+    return BPQ_OK;
+}
+
+extern "C" size_t bpq_traverse_workspace_size(int64_t t, int64_t budget, int64_t total_entries) {
+    return traverse_stage_ws_bytes(t, budget, total_entries);
+}
+
+extern "C" int bpq_traverse_cells(const double *sorted_r1, const double *sorted_r2,
+                                  const int32_t *order1, const int32_t *order2,
+                                  const int64_t *offsets, int64_t t, int64_t budget,
+                                  int64_t total_entries, int32_t *vis_i, int32_t *vis_j,
+                                  int64_t *starts, int64_t *ends, int64_t *nvis_out,
+                                  void *workspace, size_t workspace_bytes, void *stream) {
+    BPQ_CHECK(budget >= 1, BPQ_ERR_INVALID, "budget must be >= 1");
+    BPQ_CHECK(t >= 1 && t < 65536, BPQ_ERR_UNSUPPORTED, "t must be in [1, 65535]");
+    BPQ_CHECK(total_entries >= 0 && total_entries <= 0xFFFFFFFFll, BPQ_ERR_UNSUPPORTED,
+              "traversal stage handles < 2^32 entries");
+    return launch_traverse_stage(sorted_r1, sorted_r2, order1, order2, offsets, t, budget,
+                                 total_entries, vis_i, vis_j, starts, ends, nvis_out, workspace,
+                                 workspace_bytes, (cudaStream_t)stream);
+}

@@ -1,0 +1,330 @@
+"""Device-resident bilayer index and the batched search entry point.
+
+``DeviceIndex`` is the B200 counterpart of the reference containers
+``MultiIndex`` (multi_index.py:100-146), ``HbpqIndex`` (hbpq.py:240-290) and
+``FbpqTables`` (fbpq.py:28-66).  It is built from exported codebooks and
+codes (reference objects, BPQI/BPQT files, or plain arrays) or encoded on the
+device from raw vectors, and answers ``search(queries, L, k)`` for a whole
+batch with one C-ABI call (bpq_search).  PyTorch only provides the device
+buffers and the stream.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+
+MAX_PARTS = 16
+MAX_CODEBOOK = 256
+
+
+def _check_fine_params(dim: int, m: int, k: int) -> None:
+    """Same rules and messages as multi_index._check_fine_params (multi_index.py:199-207)."""
+    if m < 2 or m % 2 != 0:
+        raise ValueError(f"number of parts must be even and >= 2, got {m}")
+    if m > MAX_PARTS:
+        raise ValueError(f"number of parts must be <= {MAX_PARTS}, got {m}")
+    if dim % m != 0:
+        raise ValueError(f"dimension {dim} is not divisible into {m} parts")
+    if not 1 <= k <= MAX_CODEBOOK:
+        raise ValueError(f"codebook size must be in [1, {MAX_CODEBOOK}], got {k}")
+
+
+def coarse_norms(c: np.ndarray) -> np.ndarray:
+    """einsum('ij,ij->i') exactly as coarse_scan / build_tables_from compute it."""
+    c = np.ascontiguousarray(c, np.float32)
+    return np.einsum("ij,ij->i", c, c)
+
+
+def build_tables_host(c1, c2, books):
+    """Query-independent FBPQ tables (build_tables_from, fbpq.py:79-101):
+    (coarse_norms1, coarse_norms2, fine_norms, cross1, cross2)."""
+    c1 = np.ascontiguousarray(c1, np.float32)
+    c2 = np.ascontiguousarray(c2, np.float32)
+    books = np.ascontiguousarray(books, np.float32)
+    m, k, ds = books.shape
+    m2 = m // 2
+    t = c1.shape[0]
+    fine_norms = np.einsum("mkj,mkj->mk", books, books)
+    cross1 = np.empty((t, m2, k), np.float32)
+    cross2 = np.empty((t, m2, k), np.float32)
+    for p in range(m2):
+        cross1[:, p, :] = c1[:, p * ds : (p + 1) * ds] @ books[p].T
+        cross2[:, p, :] = c2[:, p * ds : (p + 1) * ds] @ books[m2 + p].T
+    return coarse_norms(c1), coarse_norms(c2), fine_norms, cross1, cross2
+
+
+@dataclass
+class SearchResult:
+    """Batched result.  ``ids`` holds uint32 point ids in an int32 tensor
+    (padding 0xFFFFFFFF reads as -1); ``dists`` are squared distances padded
+    with +inf; ``counts`` is the valid prefix length per query (reference
+    lists are unpadded).  Note the (dists, ids) order of the
+    batched API versus the reference's per-query (ids, dists)."""
+
+    dists: "object"
+    ids: "object"
+    counts: "object"
+    ncand: "object" = None
+
+    def numpy(self):
+        return (
+            self.dists.cpu().numpy(),
+            self.ids.cpu().numpy().view(np.uint32),
+            self.counts.cpu().numpy(),
+        )
+
+
+def _u32_tensor(a, device):
+    import torch
+
+    a = np.ascontiguousarray(a)
+    if a.dtype == np.int64:
+        if a.size and (a.min() < 0 or a.max() > 0xFFFFFFFF):
+            raise ValueError("values must fit uint32")
+        a = a.astype(np.uint32)
+    return torch.from_numpy(np.ascontiguousarray(a, np.uint32).view(np.int32)).to(device)
+
+
+def _f32(a, device):
+    import torch
+
+    if a is None:
+        return None
+    if isinstance(a, torch.Tensor):
+        return a.to(device=device, dtype=torch.float32).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(device)
+
+
+class DeviceIndex:
+    """Immutable device index; safe for concurrent searches on different
+    streams as long as each uses its own workspace (``workspace=``)."""
+
+    def __init__(self, *, c1, c2, offsets, ids, codes, books=None, tables=None, bank1=None,
+                 bank2=None, global_offsets=None, device=None, num_entries_global=None):
+        import torch
+
+        self.device = torch.device(device if device is not None else "cuda")
+        c1n = c1.detach().cpu().numpy() if isinstance(c1, torch.Tensor) else np.asarray(c1, np.float32)
+        c2n = c2.detach().cpu().numpy() if isinstance(c2, torch.Tensor) else np.asarray(c2, np.float32)
+        if c1n.shape != c2n.shape or c1n.ndim != 2:
+            raise ValueError("the two coarse codebooks must have equal shape (t, d/2)")
+        self.t, dh = c1n.shape
+        self.dim = 2 * dh
+        codes_t = codes if isinstance(codes, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(codes, np.uint8))
+        if codes_t.dim() != 2:
+            raise ValueError("codes must have shape (n, m)")
+        self.m = codes_t.shape[1]
+        self.kind = "hbpq" if bank1 is not None else "global"
+        if self.kind == "hbpq":
+            self.k = (bank1.shape[2])
+        elif books is not None:
+            self.k = books.shape[1]
+        else:
+            raise ValueError("an index needs fine codebooks or a local codebook bank")
+        _check_fine_params(self.dim, self.m, self.k)
+        # traversal keys use the reference's coarse norms (einsum, multi_index.py:285-286)
+        if tables is not None:
+            cn1, cn2 = _table_attr(tables, 0), _table_attr(tables, 1)
+        else:
+            cn1, cn2 = coarse_norms(c1n), coarse_norms(c2n)
+        dev = self.device
+        self.c1 = _f32(c1n, dev)
+        self.c2 = _f32(c2n, dev)
+        self.cn1 = _f32(cn1, dev)
+        self.cn2 = _f32(cn2, dev)
+        if isinstance(offsets, torch.Tensor):
+            self.offsets = offsets.to(dev)
+            n_off = offsets.shape[0]
+        else:
+            offs = np.asarray(offsets)
+            if offs.ndim != 1 or offs.shape[0] != self.t * self.t + 1:
+                raise ValueError("cell table size does not match the coarse codebooks")
+            if offs[0] != 0 or np.any(np.diff(offs.astype(np.int64)) < 0):
+                raise ValueError("offsets must start at 0 and be non-decreasing")
+            self.offsets = _u32_tensor(offs, dev)
+            n_off = offs.shape[0]
+        if n_off != self.t * self.t + 1:
+            raise ValueError("cell table size does not match the coarse codebooks")
+        self.ids = ids.to(dev) if isinstance(ids, torch.Tensor) else _u32_tensor(np.asarray(ids, np.uint32), dev)
+        self.codes = codes_t.to(dev).contiguous()
+        self.n = self.codes.shape[0]
+        if self.ids.shape[0] != self.n:
+            raise ValueError("entry count does not match the cell table")
+        self.global_offsets = None
+        if global_offsets is not None:
+            self.global_offsets = (global_offsets.to(dev) if isinstance(global_offsets, torch.Tensor)
+                                   else _u32_tensor(np.asarray(global_offsets), dev))
+        self.n_global = int(num_entries_global) if num_entries_global is not None else self.n
+        self.books = _f32(books, dev)
+        self.fine_norms = self.cross1 = self.cross2 = None
+        if books is not None:
+            if tables is None:
+                tables = build_tables_host(c1n, c2n, books.cpu().numpy() if isinstance(books, torch.Tensor) else books)
+            self.fine_norms = _f32(_table_attr(tables, 2), dev)
+            self.cross1 = _f32(_table_attr(tables, 3), dev)
+            self.cross2 = _f32(_table_attr(tables, 4), dev)
+        self.bank1 = _f32(bank1, dev)
+        self.bank2 = _f32(bank2, dev)
+        self._handle = None
+        self._ws = None
+        self._create()
+
+    # ------------------------------------------------------------- C handle
+    def _create(self):
+        lib = _lib.load()
+        d = _lib.IndexDesc()
+        d.dim, d.num_coarse, d.num_parts, d.codebook_size = self.dim, self.t, self.m, self.k
+        d.num_entries = self.n
+        d.num_entries_global = self.n_global
+        d.coarse1, d.coarse2 = _lib.ptr(self.c1), _lib.ptr(self.c2)
+        d.coarse_norms1, d.coarse_norms2 = _lib.ptr(self.cn1), _lib.ptr(self.cn2)
+        d.cell_offsets = _lib.ptr(self.offsets)
+        d.global_offsets = _lib.ptr(self.global_offsets)
+        d.ids, d.codes = _lib.ptr(self.ids), _lib.ptr(self.codes)
+        d.fine_books, d.fine_norms = _lib.ptr(self.books), _lib.ptr(self.fine_norms)
+        d.cross1, d.cross2 = _lib.ptr(self.cross1), _lib.ptr(self.cross2)
+        d.bank1, d.bank2 = _lib.ptr(self.bank1), _lib.ptr(self.bank2)
+        h = ctypes.c_void_p()
+        _lib.check(lib.bpq_index_create(ctypes.byref(d), 0, ctypes.byref(h)), "bpq_index_create")
+        self._handle = h
+
+    def __del__(self):
+        h = getattr(self, "_handle", None)
+        if h is not None and _lib._lib is not None:
+            _lib._lib.bpq_index_destroy(h)
+            self._handle = None
+
+    # ------------------------------------------------------------ properties
+    @property
+    def num_points(self) -> int:
+        return self.n
+
+    @property
+    def num_coarse(self) -> int:
+        return self.t
+
+    @property
+    def num_parts(self) -> int:
+        return self.m
+
+    @property
+    def codebook_size(self) -> int:
+        return self.k
+
+    @property
+    def bytes_per_point(self) -> int:
+        return 4 + self.m
+
+    def engines(self):
+        return ("hbpq",) if self.kind == "hbpq" else ("baseline", "fbpq")
+
+    # --------------------------------------------------------------- search
+    def workspace_bytes(self, engine: str, nq: int, L: int, k: int) -> int:
+        lib = _lib.load()
+        return int(lib.bpq_search_workspace_size(self._handle, _lib.ENGINES[engine], nq, L, k))
+
+    def make_workspace(self, engine: str, nq: int, L: int, k: int):
+        import torch
+
+        return torch.empty(self.workspace_bytes(engine, nq, L, k), dtype=torch.uint8, device=self.device)
+
+    def search(self, queries, L: int, k: int, engine: str = "fbpq", *, out=None, workspace=None,
+               stream=None, ncand: bool = False, popped=None, stage_events=None) -> SearchResult:
+        """Batched search: queries [nq, D] (torch on this device, or array-like
+        copied in).  Returns a SearchResult of device tensors; stream-ordered
+        on ``stream`` (default: torch's current stream), no host sync."""
+        import torch
+
+        if engine not in _lib.ENGINES:
+            raise ValueError(f"unknown engine {engine!r}")
+        if engine == "hbpq" and self.kind != "hbpq":
+            raise ValueError("engine hbpq requires an index built with local codebooks")
+        if engine != "hbpq" and self.kind == "hbpq":
+            raise ValueError(f"engine {engine} is incompatible with a local-codebook index")
+        if L < 1:
+            raise ValueError(f"budget must be >= 1, got {L}")
+        if k < 1:
+            raise ValueError(f"r must be >= 1, got {k}")
+        if not isinstance(queries, torch.Tensor):
+            queries = torch.from_numpy(np.ascontiguousarray(np.atleast_2d(queries), np.float32))
+        queries = queries.to(device=self.device, dtype=torch.float32).contiguous()
+        if queries.dim() == 1:
+            queries = queries[None]
+        if queries.shape[1] != self.dim:
+            raise ValueError(f"dimension mismatch: vectors {queries.shape[1]}, index {self.dim}")
+        nq = queries.shape[0]
+        if out is None:
+            out = SearchResult(
+                torch.empty((nq, k), dtype=torch.float32, device=self.device),
+                torch.empty((nq, k), dtype=torch.int32, device=self.device),
+                torch.empty((nq,), dtype=torch.int32, device=self.device),
+                torch.empty((nq,), dtype=torch.int64, device=self.device) if ncand else None,
+            )
+        need = self.workspace_bytes(engine, nq, L, k)
+        if workspace is None:
+            if self._ws is None or self._ws.numel() < need:
+                self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+            workspace = self._ws
+        elif workspace.numel() < need:
+            raise ValueError(f"workspace too small: {workspace.numel()} < {need}")
+        lib = _lib.load()
+        ev = None
+        if stage_events is not None:
+            ev = (ctypes.c_void_p * 4)(*[e.cuda_event for e in stage_events])
+        rc = lib.bpq_search_ex(
+            self._handle, _lib.ENGINES[engine], _lib.ptr(queries), nq, int(L), int(k),
+            _lib.ptr(out.dists), _lib.ptr(out.ids), _lib.ptr(out.counts), _lib.ptr(out.ncand),
+            _lib.ptr(popped), ev, _lib.ptr(workspace), workspace.numel(), _lib.stream_ptr(stream),
+        )
+        _lib.check(rc, "bpq_search")
+        return out
+
+    # --------------------------------------------------------- constructors
+    @classmethod
+    def from_reference(cls, index, tables=None, device=None):
+        """From a reference-layout MultiIndex / HbpqIndex (duck-typed: any
+        object with .coarse.book1.centroids, .cells.offsets, .ids, .codes and
+        .fine.codebooks or .bank.books1/.books2), plus optional FbpqTables."""
+        coarse = index.coarse
+        if getattr(coarse, "rotation", None) is not None:
+            raise NotImplementedError("OPQ-rotated coarse pairs are not supported yet (SURVEY §8f f3)")
+        c1 = coarse.book1.centroids
+        c2 = coarse.book2.centroids
+        bank = getattr(index, "bank", None)
+        kw = dict(c1=c1, c2=c2, offsets=index.cells.offsets, ids=index.ids, codes=index.codes, device=device)
+        if bank is not None:
+            if bank.rot1 is not None or bank.rot2 is not None:
+                raise NotImplementedError("rotated local banks are not supported yet (SURVEY §8f f3)")
+            return cls(bank1=bank.books1, bank2=bank.books2, **kw)
+        tab = None
+        if tables is not None:
+            tab = (tables.coarse_norms1, tables.coarse_norms2, tables.fine_norms, tables.cross1, tables.cross2)
+        return cls(books=index.fine.codebooks, tables=tab, **kw)
+
+    @classmethod
+    def load(cls, index_path, tables_path=None, device=None):
+        """From BPQI (+ optional BPQT) files (storage.py:253-360 layout)."""
+        from . import storage
+
+        rec = storage.load_index_arrays(index_path)
+        tab = storage.load_tables_arrays(tables_path) if tables_path is not None else None
+        if rec["rotation"] is not None:
+            raise NotImplementedError("OPQ-rotated indexes are not supported yet (SURVEY §8f f3)")
+        kw = dict(c1=rec["c1"], c2=rec["c2"], offsets=rec["offsets"], ids=rec["ids"], codes=rec["codes"], device=device)
+        if rec["bank1"] is not None:
+            if rec["rot1"] is not None or rec["rot2"] is not None:
+                raise NotImplementedError("rotated local banks are not supported yet (SURVEY §8f f3)")
+            return cls(bank1=rec["bank1"], bank2=rec["bank2"], **kw)
+        return cls(books=rec["books"], tables=tab, **kw)
+
+
+def _table_attr(tables, i):
+    names = ("coarse_norms1", "coarse_norms2", "fine_norms", "cross1", "cross2")
+    if isinstance(tables, (tuple, list)):
+        return tables[i]
+    return getattr(tables, names[i])

@@ -1,0 +1,210 @@
+"""GPU parity: the CUDA engine (through the C ABI) against the oracle and the
+reference-generated golden fixtures."""
+
+import numpy as np
+import pytest
+
+from parity import check_topk
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+@pytest.fixture(scope="module")
+def kernels(torch_cuda):
+    from paper_1404_1831_b200 import kernels as k
+
+    return k
+
+
+@pytest.fixture(scope="module")
+def c0_index(torch_cuda, c0):
+    from paper_1404_1831_b200 import DeviceIndex
+
+    tables = (c0["cn1"], c0["cn2"], c0["fine_norms"], c0["cross1"], c0["cross2"])
+    return DeviceIndex(c1=c0["c1"], c2=c0["c2"], offsets=c0["offsets"], ids=c0["ids"], codes=c0["codes"],
+                       books=c0["books"], tables=tables)
+
+
+# ---------------------------------------------------------------- stage level
+def test_traverse_stage_known_answers(kat, kernels):
+    """traverse_cells on the GPU == the reference's numba output, element for element."""
+    for n in range(int(kat["n_traverse"])):
+        p = f"tr{n}_"
+        got = kernels.traverse_cells(kat[p + "sr1"], kat[p + "sr2"], kat[p + "o1"], kat[p + "o2"],
+                                     kat[p + "off"], int(kat[p + "budget"]))
+        for g, name in zip(got, ("vi", "vj", "st", "en")):
+            np.testing.assert_array_equal(g, kat[p + name], err_msg=f"case {n} {name}")
+
+
+def test_traverse_stage_c0(c0, kernels, oracle):
+    for x in range(6):
+        p = f"stage{x}_"
+        sr1, sr2, o1, o2 = oracle.sort_halves(c0[p + "r1"], c0[p + "r2"])
+        got = kernels.traverse_cells(sr1, sr2, o1, o2, c0["offsets"], 10_000)
+        for g, name in zip(got, ("vi", "vj", "st", "en")):
+            np.testing.assert_array_equal(g, c0[p + name])
+
+
+def test_scan_stages_bit_exact(c0, kernels):
+    dh = c0["c1"].shape[1]
+    for x in range(6):
+        p = f"stage{x}_"
+        vis = (c0[p + "vi"], c0[p + "vj"], c0[p + "st"], c0[p + "en"])
+        ti, td = kernels.scan_tables(*vis, c0["ids"], c0["codes"], c0[p + "q_norm"], c0[p + "dots1"],
+                                     c0[p + "dots2"], c0["cn1"], c0["cn2"], c0[p + "fold"], c0["cross1"],
+                                     c0["cross2"])
+        np.testing.assert_array_equal(ti, c0[p + "tab_ids"])
+        np.testing.assert_array_equal(td.view(np.uint32), c0[p + "tab_d"].view(np.uint32))
+        q = c0["queries"][x].astype(np.float32)
+        gi, gd = kernels.scan_global(*vis, c0["ids"], c0["codes"], q[None, :dh] - c0["c1"],
+                                     q[None, dh:] - c0["c2"], c0["books"])
+        np.testing.assert_array_equal(gd.view(np.uint32), c0[p + "glob_d"].view(np.uint32))
+
+
+def test_scan_local_bit_exact(hbpq_rig, kernels, oracle):
+    g = hbpq_rig
+    q = g["queries"][0].astype(np.float32)
+    qr, _, _, r1, r2 = oracle.coarse_scan(g["c1"], g["c2"], q)
+    vis = oracle.traverse(g["offsets"], r1, r2, 2000)
+    dh = g["c1"].shape[1]
+    ci, cd = kernels.scan_local(*vis, g["ids"], g["hcodes"], qr[None, :dh] - g["c1"], qr[None, dh:] - g["c2"],
+                                g["bank1"], g["bank2"])
+    np.testing.assert_array_equal(ci, g["stage_local_ids"])
+    np.testing.assert_array_equal(cd.view(np.uint32), g["stage_local_d"].view(np.uint32))
+
+
+def test_empty_visit_stage(kernels):
+    e = np.empty(0, np.int32)
+    ids, d = kernels.scan_tables(e, e, np.empty(0, np.int64), np.empty(0, np.int64), np.zeros(3, np.uint32),
+                                 np.zeros((3, 2), np.uint8), 1.0, np.zeros(2, np.float32), np.zeros(2, np.float32),
+                                 np.zeros(2, np.float32), np.zeros(2, np.float32), np.zeros((2, 4), np.float32),
+                                 np.zeros((2, 1, 4), np.float32), np.zeros((2, 1, 4), np.float32))
+    assert ids.size == 0 and d.size == 0
+
+
+# ------------------------------------------------------------------ end to end
+def _qn(q):
+    return np.einsum("ij,ij->i", q.astype(np.float64), q.astype(np.float64))
+
+
+@pytest.mark.parametrize("engine,nq,L,k", [("fbpq", 1000, 10_000, 100), ("baseline", 200, 10_000, 100),
+                                           ("fbpq", 200, 1_000, 10), ("baseline", 200, 1_000, 10)])
+def test_search_c0_vs_reference(c0, c0_index, engine, nq, L, k):
+    q = c0["queries"][:nq].astype(np.float32)
+    res = c0_index.search(q, L, k, engine, ncand=True)
+    d, i, c = res.numpy()
+    tag = f"{engine}_L{L}_k{k}"
+    want_c = np.minimum(k, c0[tag + "_ncand"][:nq])
+    check_topk(d, i, c, c0[tag + "_d"][:nq], c0[tag + "_ids"][:nq], want_c, _qn(q))
+    ncand = res.ncand.cpu().numpy()
+    assert np.mean(ncand == c0[tag + "_ncand"][:nq]) > 0.99
+
+
+def test_search_hbpq_vs_reference(hbpq_rig, torch_cuda):
+    from paper_1404_1831_b200 import DeviceIndex
+
+    g = hbpq_rig
+    dix = DeviceIndex(c1=g["c1"], c2=g["c2"], offsets=g["offsets"], ids=g["ids"], codes=g["hcodes"],
+                      bank1=g["bank1"], bank2=g["bank2"])
+    q = g["queries"].astype(np.float32)
+    d, i, c = dix.search(q, 2000, 50, "hbpq").numpy()
+    want_c = (g["hbpq_ids"] != 0xFFFFFFFF).sum(1)
+    check_topk(d, i, c, g["hbpq_d"], g["hbpq_ids"], want_c, _qn(q))
+
+
+def test_per_query_api_matches_batch(c0, c0_index):
+    import paper_1404_1831_b200 as bpq
+
+    q = c0["queries"][3].astype(np.float32)
+    ids, d = bpq.search_fbpq(c0_index, None, q, 10_000, 100)
+    bd, bi, bc = c0_index.search(q[None], 10_000, 100, "fbpq").numpy()
+    assert ids.dtype == np.uint32 and d.dtype == np.float32
+    np.testing.assert_array_equal(ids, bi[0, : bc[0]])
+    with pytest.raises(ValueError):
+        bpq.search_fbpq(c0_index, None, q, 10_000, 0)
+    with pytest.raises(ValueError):
+        c0_index.search(q[None], 0, 10, "fbpq")
+    with pytest.raises(ValueError):
+        c0_index.search(q[None], 10, 10, "hbpq")
+
+
+def test_search_vs_oracle_small_synthetic(torch_cuda, oracle):
+    """Random small index incl. empty cells, budgets below/above N, k > candidates."""
+    from paper_1404_1831_b200 import DeviceIndex
+
+    rng = np.random.default_rng(7)
+    t, dim, m, kk, n = 24, 32, 4, 16, 3000
+    c1 = rng.normal(size=(t, dim // 2)).astype(np.float32)
+    c2 = rng.normal(size=(t, dim // 2)).astype(np.float32)
+    books = rng.normal(scale=0.2, size=(m, kk, dim // m)).astype(np.float32)
+    base = rng.normal(size=(n, dim)).astype(np.float32)
+    off, ids, codes = oracle.build_index(base, c1, c2, books)
+    idx = oracle.Index(c1, c2, off, ids, codes, books=books)
+    dix = DeviceIndex(c1=c1, c2=c2, offsets=off, ids=ids, codes=codes, books=books, tables=idx.tables)
+    q = rng.normal(size=(64, dim)).astype(np.float32)
+    for engine in ("fbpq", "baseline"):
+        for L, k in ((1, 1), (37, 5), (500, 50), (5000, 100), (n, 1000)):
+            wd, wi, wc, _ = oracle.search_batch_numpy(idx, engine, q, L, k)
+            d, i, c = dix.search(q, L, k, engine).numpy()
+            check_topk(d, i, c, wd, wi, wc, _qn(q), min_exact_frac=0.95)
+
+
+def test_empty_index_returns_nothing(torch_cuda):
+    from paper_1404_1831_b200 import DeviceIndex
+
+    t, dim, m = 4, 8, 2
+    rng = np.random.default_rng(1)
+    dix = DeviceIndex(c1=rng.normal(size=(t, 4)), c2=rng.normal(size=(t, 4)), offsets=np.zeros(t * t + 1, np.int64),
+                      ids=np.zeros(0, np.uint32), codes=np.zeros((0, m), np.uint8),
+                      books=rng.normal(size=(m, 8, 4)).astype(np.float32))
+    d, i, c = dix.search(rng.normal(size=(3, dim)).astype(np.float32), 10, 5, "fbpq").numpy()
+    assert (c == 0).all() and np.isinf(d).all() and (i == 0xFFFFFFFF).all()
+
+
+def test_sharded_global_budget_equals_single(c0, torch_cuda):
+    """Shards built with id offsets + global counts: merged top-k == 1-index top-k."""
+    import torch
+
+    from paper_1404_1831_b200 import DeviceIndex, sharded
+    from oracle import oracle as orc
+
+    q = c0["queries"][:100].astype(np.float32)
+    tables = (c0["cn1"], c0["cn2"], c0["fine_norms"], c0["cross1"], c0["cross2"])
+    full = DeviceIndex(c1=c0["c1"], c2=c0["c2"], offsets=c0["offsets"], ids=c0["ids"], codes=c0["codes"],
+                       books=c0["books"], tables=tables)
+    want = full.search(q, 10_000, 100, "fbpq").numpy()
+    shards = sharded.split_index_arrays(c0["offsets"], c0["ids"], c0["codes"], 3)
+    outs = []
+    for s in shards:
+        dix = DeviceIndex(c1=c0["c1"], c2=c0["c2"], offsets=s["offsets"], ids=s["ids"], codes=s["codes"],
+                          books=c0["books"], tables=tables, global_offsets=c0["offsets"],
+                          num_entries_global=int(c0["offsets"][-1]))
+        outs.append(dix.search(q, 10_000, 100, "fbpq"))
+    merged = sharded.merge_results([o.dists for o in outs], [o.ids for o in outs], [o.counts for o in outs], 100)
+    got = merged.numpy()
+    np.testing.assert_array_equal(got[1], want[1])
+    np.testing.assert_array_equal(got[0], want[0])
+    np.testing.assert_array_equal(got[2], want[2])
+
+
+def test_device_encoding_matches_reference(c0, torch_cuda):
+    from paper_1404_1831_b200 import encode
+
+    x = c0["enc_x"].astype(np.float32)
+    dix = encode.build_index(x, c0["c1"], c0["c2"], c0["books"], id_offset=77)
+    off = dix.offsets.cpu().numpy().view(np.uint32).astype(np.int64)
+    ids = dix.ids.cpu().numpy().view(np.uint32)
+    codes = dix.codes.cpu().numpy()
+    # near-tie argmins may move a row; require near-identity and exact layout rules
+    assert np.mean(off == c0["enc_offsets"]) > 0.99
+    assert np.mean(ids == c0["enc_ids"]) > 0.99
+    assert np.mean(np.all(codes == c0["enc_codes"], axis=1)) > 0.99
+    assert off[-1] == x.shape[0] and np.all(np.diff(off) >= 0)
