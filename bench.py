@@ -293,6 +293,9 @@ def main():
     torch.cuda.synchronize()
 
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    for row in evs:  # torch creates CUDA events lazily on first record
+        for e in row:
+            e.record(stream)
     if world > 1:
         import torch.distributed as dist
 

@@ -36,6 +36,13 @@ def check_topk(got_d, got_i, got_c, want_d, want_i, want_c, qnorm2=None, rtol=RT
             continue
         if np.array_equal(got_i[q, :n], want_i[q, :n]):
             exact += 1
+        elif n:
+            # away from the k-th distance the id SETS must agree exactly
+            thr = wd[n - 1] * (1.0 - 2.0 * rtol) - floor
+            gs = set(got_i[q, :n][gd < thr].tolist())
+            ws = set(want_i[q, :n][wd < thr].tolist())
+            if gs != ws:
+                bad.append((q, "set", sorted(gs ^ ws)[:5]))
         # id mismatches are tolerated only where the rank's distance is a near-tie,
         # which the elementwise distance check above already bounds.
     assert not bad, f"{len(bad)} queries violate the contract, first: {bad[:5]}"
