@@ -11,7 +11,7 @@ import os
 from pathlib import Path
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libbpq_b200.so"
+LIB_PATH = Path(os.environ["BPQ_LIB"]) if os.environ.get("BPQ_LIB") else _PKG / "libbpq_b200.so"
 
 ENGINE_BASELINE, ENGINE_FBPQ, ENGINE_HBPQ = 0, 1, 2
 ENGINES = {"baseline": ENGINE_BASELINE, "fbpq": ENGINE_FBPQ, "hbpq": ENGINE_HBPQ}

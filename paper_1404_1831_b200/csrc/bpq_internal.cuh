@@ -29,8 +29,8 @@ int fail(int code, const std::string &msg);
 // Tunables of the fused traversal + scan + top-k kernel.
 constexpr int kSearchThreads = 256;     // threads per CTA (one CTA per query at a time)
 constexpr int kTopkBuf = 2048;          // per-CTA top-k candidate buffer (u64 keys)
-constexpr int kMaxK = kTopkBuf - kSearchThreads;  // largest k the engine accepts
-constexpr int kSortCap = 1024;          // final-band cells sorted in shared memory
+constexpr int kMaxK = kTopkBuf - 4 * kSearchThreads;  // largest k the engine accepts
+constexpr int kSortCap = 512;           // final-band cells sorted in shared memory
 constexpr int kBandCap = 32768;         // max cells enumerated per band
 constexpr int kMaxDim = 1024;           // queries staged in shared memory
 

@@ -99,7 +99,7 @@ extern "C" int bpq_index_create(const bpq_index_desc *d, int copy_from_host, bpq
     BPQ_CHECK(d->num_entries_global >= d->num_entries && d->num_entries_global <= 0xFFFFFFFFll,
               BPQ_ERR_INVALID, "global entry count must be >= local and fit uint32");
     BPQ_CHECK(d->coarse1 && d->coarse2 && d->coarse_norms1 && d->coarse_norms2 && d->cell_offsets &&
-                  d->ids && d->codes,
+                  ((d->ids && d->codes) || d->num_entries == 0),
               BPQ_ERR_INVALID, "coarse books, norms, offsets, ids and codes are required");
     bpq_index *h = new bpq_index();
     Index &ix = h->ix;
@@ -193,7 +193,7 @@ extern "C" int bpq_search_ex(const bpq_index *index, int engine, const float *qu
     // traverse() rejects budget < 1 (multi_index.py:308-309); search_* reject r < 1
     BPQ_CHECK(budget >= 1, BPQ_ERR_INVALID, "budget must be >= 1");
     BPQ_CHECK(k >= 1, BPQ_ERR_INVALID, "r must be >= 1");
-    BPQ_CHECK(k <= kMaxK, BPQ_ERR_UNSUPPORTED, "k exceeds the engine's top-k buffer (1792)");
+    BPQ_CHECK(k <= kMaxK, BPQ_ERR_UNSUPPORTED, "k exceeds the engine's top-k buffer (1024)");
     BPQ_CHECK(nq >= 0, BPQ_ERR_INVALID, "nq must be >= 0");
     switch (engine) {
         case BPQ_ENGINE_BASELINE:
