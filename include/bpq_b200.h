@@ -71,6 +71,13 @@ typedef struct bpq_index_desc {
     const float *fine_norms;        /* [M, K]               fbpq */
     const float *cross1, *cross2;   /* [T, M/2, K]          fbpq */
     const float *bank1, *bank2;     /* [T, M/2, K, D/M]     hbpq */
+    /* Optional populated-cell lists of the traversal table (global_offsets
+     * when sharded): row i's populated columns ascending and column j's
+     * populated rows ascending (bpq_build_cell_lists).  With them the
+     * traversal enumerates a band segment through the list whenever the
+     * line holds fewer populated cells than the segment has cells. */
+    const uint32_t *row_ptr, *col_ptr;   /* [T+1] */
+    const uint16_t *row_cols, *col_rows; /* [min(N_global, T*T)] capacity */
 } bpq_index_desc;
 
 typedef struct bpq_index bpq_index;
@@ -157,6 +164,14 @@ int bpq_pack_cells(const int64_t *i_idx, const int64_t *j_idx, int64_t n, int32_
                    uint32_t id_offset, const uint8_t *codes_in, int32_t m,
                    uint32_t *out_offsets, uint32_t *out_ids, uint8_t *out_codes,
                    void *workspace, size_t workspace_bytes, void *stream);
+
+/* Build the populated-cell lists of a cell table (device pointers): counts
+ * per row/column, exclusive scans, ordered fills.  row_cols / col_rows need
+ * capacity for every populated cell (min(entries, t*t) suffices). */
+size_t bpq_cell_lists_workspace_size(int32_t t);
+int bpq_build_cell_lists(const uint32_t *offsets, int32_t t, uint32_t *row_ptr, uint16_t *row_cols,
+                         uint32_t *col_ptr, uint16_t *col_rows, void *workspace,
+                         size_t workspace_bytes, void *stream);
 
 /* Merge per-shard top-k lists [g, nq, k] into [nq, k] by (dist, id). */
 int bpq_merge_topk(const float *dists, const uint32_t *ids, const int32_t *counts, int32_t g,

@@ -47,6 +47,10 @@ class IndexDesc(ctypes.Structure):
         ("cross2", P),
         ("bank1", P),
         ("bank2", P),
+        ("row_ptr", P),
+        ("col_ptr", P),
+        ("row_cols", P),
+        ("col_rows", P),
     ]
 
 
@@ -69,6 +73,8 @@ SIGNATURES = {
     "bpq_encode_local": (ctypes.c_int, [P, I64, I32, P, P, P, P, P, P, I32, I32, P, P]),
     "bpq_pack_workspace_size": (SZ, [I64, I32]),
     "bpq_pack_cells": (ctypes.c_int, [P, P, I64, I32, ctypes.c_uint32, P, I32, P, P, P, P, SZ, P]),
+    "bpq_cell_lists_workspace_size": (SZ, [I32]),
+    "bpq_build_cell_lists": (ctypes.c_int, [P, I32, P, P, P, P, P, SZ, P]),
     "bpq_merge_topk": (ctypes.c_int, [P, P, P, I32, I64, I32, P, P, P, P]),
 }
 

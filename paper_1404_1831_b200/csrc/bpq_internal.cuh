@@ -31,6 +31,7 @@ constexpr int kSearchThreads = 256;     // threads per CTA (one CTA per query at
 constexpr int kTopkBuf = 2048;          // per-CTA top-k candidate buffer (u64 keys)
 constexpr int kMaxK = kTopkBuf - 4 * kSearchThreads;  // largest k the engine accepts
 constexpr int kSortCap = 512;           // final-band cells sorted in shared memory
+constexpr int kLutMin = 96;             // cells with >= this many entries are scanned via a smem LUT
 constexpr int kBandCap = 32768;         // max cells enumerated per band
 constexpr int kMaxDim = 1024;           // queries staged in shared memory
 
@@ -43,6 +44,9 @@ struct Index {
     const uint32_t *ids;
     const uint8_t *codes;
     const float *books, *fine_norms, *cross1, *cross2, *bank1, *bank2;
+    // populated-cell lists (optional): row i -> columns j, column j -> rows i
+    const uint32_t *rowptr, *colptr;
+    const uint16_t *rowcols, *colrows;
     std::vector<void *> owned;
 };
 
@@ -52,11 +56,12 @@ int launch_coarse_dots(const float *queries, int64_t nq, int32_t D, const float 
                        cudaStream_t stream);
 int launch_row_sort(const float *queries, int64_t nq, int32_t D, const float *dots1,
                     const float *dots2, const float *cn1, const float *cn2, int32_t T,
-                    float *sr1, float *sr2, int32_t *ord1, int32_t *ord2, cudaStream_t stream);
+                    float *sr1, float *sr2, int32_t *ord1, int32_t *ord2, int32_t *pos1,
+                    int32_t *pos2, cudaStream_t stream);
 
 struct SearchWorkspace {
     float *dots1, *dots2, *sr1, *sr2;
-    int32_t *ord1, *ord2;
+    int32_t *ord1, *ord2, *pos1, *pos2;
     unsigned int *counter;
     char *cta_scratch;
     size_t cta_stride;

@@ -22,13 +22,13 @@ size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct SearchLayout {
     int64_t chunk;
-    size_t dots1, dots2, sr1, sr2, ord1, ord2, counter, cta, cta_stride, total;
+    size_t dots1, dots2, sr1, sr2, ord1, ord2, pos1, pos2, counter, cta, cta_stride, total;
     int n_cta;
 };
 
 int64_t query_chunk(int64_t nq, int32_t T) {
-    // keep the per-chunk first-layer buffers (6 arrays of [chunk, T] x 4 B) near 2 GiB
-    int64_t per_q = (int64_t)T * 24;
+    // keep the per-chunk first-layer buffers (8 arrays of [chunk, T] x 4 B) near 2 GiB
+    int64_t per_q = (int64_t)T * 32;
     int64_t c = ((int64_t)2 << 30) / per_q;
     c = std::max<int64_t>(c, 256);
     return std::max<int64_t>(1, std::min<int64_t>(nq, c));
@@ -48,6 +48,8 @@ bool layout_for(const Index &ix, int64_t nq, SearchLayout *L) {
     s.sr2 = o; o += al(row);
     s.ord1 = o; o += al(row);
     s.ord2 = o; o += al(row);
+    s.pos1 = o; o += al(row);
+    s.pos2 = o; o += al(row);
     s.counter = o; o += al(4);
     s.cta_stride = al(search_cta_scratch_bytes(ix.T));
     s.cta = o; o += s.cta_stride * n_cta;
@@ -96,6 +98,10 @@ extern "C" int bpq_index_create(const bpq_index_desc *d, int copy_from_host, bpq
     BPQ_CHECK(d->dim <= kMaxDim, BPQ_ERR_UNSUPPORTED, "dim > 1024 exceeds the search kernel");
     BPQ_CHECK(d->num_entries >= 0 && d->num_entries <= 0xFFFFFFFFll, BPQ_ERR_UNSUPPORTED,
               "entries must fit uint32 offsets");
+    BPQ_CHECK((d->row_ptr == nullptr) == (d->col_ptr == nullptr) &&
+                  (d->row_ptr == nullptr) == (d->row_cols == nullptr) &&
+                  (d->row_ptr == nullptr) == (d->col_rows == nullptr),
+              BPQ_ERR_INVALID, "cell lists must be given all together or not at all");
     BPQ_CHECK(d->num_entries_global >= d->num_entries && d->num_entries_global <= 0xFFFFFFFFll,
               BPQ_ERR_INVALID, "global entry count must be >= local and fit uint32");
     BPQ_CHECK(d->coarse1 && d->coarse2 && d->coarse_norms1 && d->coarse_norms2 && d->cell_offsets &&
@@ -127,6 +133,10 @@ extern "C" int bpq_index_create(const bpq_index_desc *d, int copy_from_host, bpq
         ix.cross2 = d->cross2;
         ix.bank1 = d->bank1;
         ix.bank2 = d->bank2;
+        ix.rowptr = d->row_ptr;
+        ix.rowcols = d->row_cols;
+        ix.colptr = d->col_ptr;
+        ix.colrows = d->col_rows;
     } else {
         int rc = 0;
         rc |= copy_in(d->coarse1, T * dh, ix.owned, &ix.c1);
@@ -147,6 +157,15 @@ extern "C" int bpq_index_create(const bpq_index_desc *d, int copy_from_host, bpq
         rc |= copy_in(d->bank1, T * (M / 2) * K * ds, ix.owned, &ix.bank1);
         rc |= copy_in(d->bank2, T * (M / 2) * K * ds, ix.owned, &ix.bank2);
         (void)D;
+        ix.rowptr = ix.colptr = nullptr;
+        ix.rowcols = ix.colrows = nullptr;
+        if (d->row_ptr && d->col_ptr && d->row_cols && d->col_rows) {
+            const size_t P = std::min<size_t>(N > 0 ? N : 1, T * T);
+            rc |= copy_in(d->row_ptr, T + 1, ix.owned, &ix.rowptr);
+            rc |= copy_in(d->col_ptr, T + 1, ix.owned, &ix.colptr);
+            rc |= copy_in(d->row_cols, P, ix.owned, &ix.rowcols);
+            rc |= copy_in(d->col_rows, P, ix.owned, &ix.colrows);
+        }
         if (rc) {
             std::string msg = g_last_error;
             bpq_index_destroy(h);
@@ -223,6 +242,8 @@ extern "C" int bpq_search_ex(const bpq_index *index, int engine, const float *qu
     ws.sr2 = reinterpret_cast<float *>(w + L.sr2);
     ws.ord1 = reinterpret_cast<int32_t *>(w + L.ord1);
     ws.ord2 = reinterpret_cast<int32_t *>(w + L.ord2);
+    ws.pos1 = reinterpret_cast<int32_t *>(w + L.pos1);
+    ws.pos2 = reinterpret_cast<int32_t *>(w + L.pos2);
     ws.counter = reinterpret_cast<unsigned int *>(w + L.counter);
     ws.cta_scratch = w + L.cta;
     ws.cta_stride = L.cta_stride;
@@ -237,7 +258,7 @@ extern "C" int bpq_search_ex(const bpq_index *index, int engine, const float *qu
         if (rc) return rc;
         if (ev) BPQ_CUDA_TRY(cudaEventRecord((cudaEvent_t)stage_events[1], s));
         rc = launch_row_sort(qc, n, ix.D, ws.dots1, ws.dots2, ix.cn1, ix.cn2, ix.T, ws.sr1, ws.sr2,
-                             ws.ord1, ws.ord2, s);
+                             ws.ord1, ws.ord2, ws.pos1, ws.pos2, s);
         if (rc) return rc;
         if (ev) BPQ_CUDA_TRY(cudaEventRecord((cudaEvent_t)stage_events[2], s));
         rc = launch_search(ix, engine, qc, q0, n, budget, k, ws, out_dist, out_ids, out_count,

@@ -89,7 +89,8 @@ __global__ void __launch_bounds__(kSortThreads) row_sort_kernel(
     const float *__restrict__ Q, int D, const float *__restrict__ dots1,
     const float *__restrict__ dots2, const float *__restrict__ cn1,
     const float *__restrict__ cn2, int T, float *__restrict__ sr1, float *__restrict__ sr2,
-    int32_t *__restrict__ ord1, int32_t *__restrict__ ord2) {
+    int32_t *__restrict__ ord1, int32_t *__restrict__ ord2, int32_t *__restrict__ pos1,
+    int32_t *__restrict__ pos2) {
     using Sort = cub::BlockRadixSort<unsigned int, kSortThreads, ITEMS, int>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     auto &temp = *reinterpret_cast<typename Sort::TempStorage *>(smem_raw);
@@ -137,12 +138,14 @@ __global__ void __launch_bounds__(kSortThreads) row_sort_kernel(
     Sort(temp).SortBlockedToStriped(keys, vals, 0, 32);
     float *sr = (h ? sr2 : sr1) + q * T;
     int32_t *ord = (h ? ord2 : ord1) + q * T;
+    int32_t *pos = (h ? pos2 : pos1) + q * T;  // inverse permutation
 #pragma unroll
     for (int s = 0; s < ITEMS; s++) {
         int rank = s * kSortThreads + threadIdx.x;
         if (rank < T) {
             sr[rank] = __uint_as_float(keys[s]);
             ord[rank] = vals[s];
+            pos[vals[s]] = rank;
         }
     }
 }
@@ -150,7 +153,8 @@ __global__ void __launch_bounds__(kSortThreads) row_sort_kernel(
 template <int ITEMS>
 int launch_row_sort_t(const float *Q, int64_t nq, int32_t D, const float *dots1,
                       const float *dots2, const float *cn1, const float *cn2, int32_t T,
-                      float *sr1, float *sr2, int32_t *ord1, int32_t *ord2, cudaStream_t stream) {
+                      float *sr1, float *sr2, int32_t *ord1, int32_t *ord2, int32_t *pos1,
+                      int32_t *pos2, cudaStream_t stream) {
     using Sort = cub::BlockRadixSort<unsigned int, kSortThreads, ITEMS, int>;
     size_t smem = sizeof(typename Sort::TempStorage);
     static bool configured = false;
@@ -161,7 +165,7 @@ int launch_row_sort_t(const float *Q, int64_t nq, int32_t D, const float *dots1,
     }
     dim3 grid((unsigned)nq, 2);
     row_sort_kernel<ITEMS><<<grid, kSortThreads, smem, stream>>>(Q, D, dots1, dots2, cn1, cn2, T,
-                                                                 sr1, sr2, ord1, ord2);
+                                                                 sr1, sr2, ord1, ord2, pos1, pos2);
     BPQ_CUDA_TRY(cudaGetLastError());
     return BPQ_OK;
 }
@@ -180,18 +184,19 @@ int launch_coarse_dots(const float *queries, int64_t nq, int32_t D, const float 
 
 int launch_row_sort(const float *queries, int64_t nq, int32_t D, const float *dots1,
                     const float *dots2, const float *cn1, const float *cn2, int32_t T,
-                    float *sr1, float *sr2, int32_t *ord1, int32_t *ord2, cudaStream_t stream) {
+                    float *sr1, float *sr2, int32_t *ord1, int32_t *ord2, int32_t *pos1,
+                    int32_t *pos2, cudaStream_t stream) {
     if (nq == 0) return BPQ_OK;
     if (T <= kSortThreads * 1)
-        return launch_row_sort_t<1>(queries, nq, D, dots1, dots2, cn1, cn2, T, sr1, sr2, ord1, ord2, stream);
+        return launch_row_sort_t<1>(queries, nq, D, dots1, dots2, cn1, cn2, T, sr1, sr2, ord1, ord2, pos1, pos2, stream);
     if (T <= kSortThreads * 4)
-        return launch_row_sort_t<4>(queries, nq, D, dots1, dots2, cn1, cn2, T, sr1, sr2, ord1, ord2, stream);
+        return launch_row_sort_t<4>(queries, nq, D, dots1, dots2, cn1, cn2, T, sr1, sr2, ord1, ord2, pos1, pos2, stream);
     if (T <= kSortThreads * 8)
-        return launch_row_sort_t<8>(queries, nq, D, dots1, dots2, cn1, cn2, T, sr1, sr2, ord1, ord2, stream);
+        return launch_row_sort_t<8>(queries, nq, D, dots1, dots2, cn1, cn2, T, sr1, sr2, ord1, ord2, pos1, pos2, stream);
     if (T <= kSortThreads * 16)
-        return launch_row_sort_t<16>(queries, nq, D, dots1, dots2, cn1, cn2, T, sr1, sr2, ord1, ord2, stream);
+        return launch_row_sort_t<16>(queries, nq, D, dots1, dots2, cn1, cn2, T, sr1, sr2, ord1, ord2, pos1, pos2, stream);
     if (T <= kSortThreads * 32)
-        return launch_row_sort_t<32>(queries, nq, D, dots1, dots2, cn1, cn2, T, sr1, sr2, ord1, ord2, stream);
+        return launch_row_sort_t<32>(queries, nq, D, dots1, dots2, cn1, cn2, T, sr1, sr2, ord1, ord2, pos1, pos2, stream);
     return fail(BPQ_ERR_UNSUPPORTED, "num_coarse > 16384 is outside the row-sort kernel range");
 }
 

@@ -157,7 +157,8 @@ TravLayout trav_layout(int64_t t, int64_t budget, int64_t total) {
 }  // namespace
 
 size_t search_cta_scratch_bytes(int32_t T) {
-    return (((size_t)5 * T * 4 + 15) & ~(size_t)15) + (size_t)2 * kBandCap * sizeof(int4);
+    return (((size_t)6 * T * 4 + 15) & ~(size_t)15) + (size_t)2 * T * sizeof(uint4) +
+           (size_t)2 * kBandCap * sizeof(int4);
 }
 
 

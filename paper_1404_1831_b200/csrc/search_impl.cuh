@@ -64,6 +64,8 @@ struct __align__(16) Smem {
     int32_t coj[NT];
     uint32_t cstart[NT];
     float cbase[NT];
+    uint32_t ccnt[NT];
+    uint16_t bigs[NT];
     uint32_t slin[kSortCap];
     uint16_t sidx[kSortCap];
     uint32_t hist_w[256];
@@ -79,6 +81,8 @@ struct __align__(16) Smem {
     float qnorm;
     int sel_v;
     int arows;
+    int acols;
+    uint32_t nbig;
     int err;
 };
 
@@ -98,6 +102,9 @@ struct Args {
     const float *dots1, *dots2;
     const KT *sr1, *sr2;
     const int32_t *ord1, *ord2;
+    const int32_t *pos1, *pos2;
+    const uint32_t *rowptr, *colptr;
+    const uint16_t *rowcols, *colrows;
     long long L;
     int k;
     int tab_floats;  // floats of the per-query table staged after Smem
@@ -326,6 +333,15 @@ __device__ __forceinline__ void topk_compact(Smem &S, int k) {
 }
 
 // ------------------------------------------------------- per-query context
+//
+// Staircase state.  The popped region is a Young diagram in sorted
+// coordinates.  It is split on the diagonal: row a owns its cells with
+// b >= a (boundary rowB[a], initially a) and column b owns its cells with
+// a > b (boundary colB[b], initially b + 1).  Rows whose diagonal key
+// key(a, a) exceeds tau hold no cells <= tau, and likewise columns whose
+// key(b + 1, b) exceeds tau, so a count or a band touches only O(active
+// rows + active columns) lines even when the region is a long thin "L"
+// (one very close codeword per half, which the BASELINE mixture produces).
 template <int ENGINE, int M, typename KT, typename OffT>
 struct Query {
     const Args<KT, OffT> &A;
@@ -334,20 +350,25 @@ struct Query {
     const KT *sr1, *sr2;     // global sorted half-distances of this query
     const KT *s1s, *s2s;     // smem prefixes [0, P)
     const float *tab;        // smem per-query table (fold or query vector)
-    const int32_t *o1, *o2;
+    float *lut;              // smem per-cell lookup table (FBPQ)
+    const int32_t *o1, *o2;  // sorted position -> codeword
+    const int32_t *p1, *p2;  // codeword -> sorted position
     const float *d1, *d2;
     int T, P;
     unsigned long long ncand;  // uniform across the CTA
     unsigned long long popped;
 
-    __device__ Query(const Args<KT, OffT> &a, Smem &s, int64_t q, const float *tab_, const KT *s1, const KT *s2)
-        : A(a), S(s), qi(q), s1s(s1), s2s(s2), tab(tab_) {
+    __device__ Query(const Args<KT, OffT> &a, Smem &s, int64_t q, const float *tab_, float *lut_,
+                     const KT *s1, const KT *s2)
+        : A(a), S(s), qi(q), s1s(s1), s2s(s2), tab(tab_), lut(lut_) {
         T = A.T;
         P = A.sr_smem;
         sr1 = A.sr1 + q * T;
         sr2 = A.sr2 + q * T;
         o1 = A.ord1 + q * T;
         o2 = A.ord2 + q * T;
+        p1 = A.pos1 ? A.pos1 + q * T : nullptr;
+        p2 = A.pos2 ? A.pos2 + q * T : nullptr;
         d1 = A.dots1 ? A.dots1 + q * T : nullptr;
         d2 = A.dots2 ? A.dots2 + q * T : nullptr;
         ncand = 0;
@@ -373,6 +394,59 @@ struct Query {
         return (int)((lin >> (24 - 8 * (d - 8))) & 0xFF);
     }
 
+    __device__ __forceinline__ void offer(float dist, uint32_t id) {
+        const unsigned long long kk = ((unsigned long long)canon_bits(dist) << 32) | id;
+        if (kk < S.thr) {
+            uint32_t pos = atomicAdd(&S.ntk, 1u);
+            S.tk[pos] = kk;
+        }
+    }
+
+    __device__ __forceinline__ void round_end() {
+        __syncthreads();
+        if (S.ntk > (uint32_t)(kTopkBuf - NT * kUnroll)) topk_compact(S, A.k);
+    }
+
+    // FBPQ, one large cell: LUT[p][c] = fold[p][c] + 2*cross[row][p][c] is
+    // exactly the reference's per-part increment (numba_backend.py:236-240),
+    // staged once so each entry costs M shared-memory lookups.
+    __device__ void scan_cell_lut(int oi, int oj, uint32_t lst, uint32_t lc, float cb) {
+        constexpr int M2 = M / 2;
+        const int K = A.K;
+        for (int idx = threadIdx.x; idx < M * K; idx += NT) {
+            const int p = idx / K, c = idx - p * K;
+            const float x = p < M2 ? __ldg(A.cross1 + ((size_t)oi * M2 + p) * K + c)
+                                   : __ldg(A.cross2 + ((size_t)oj * M2 + (p - M2)) * K + c);
+            lut[idx] = __fadd_rn(tab[idx], __fmul_rn(2.f, x));
+        }
+        __syncthreads();
+        for (uint32_t e0 = 0; e0 < lc; e0 += NT * kUnroll) {
+            uint32_t w[kUnroll][4];
+            uint32_t idv[kUnroll];
+#pragma unroll
+            for (int u = 0; u < kUnroll; u++) {
+                const uint32_t e = e0 + u * NT + threadIdx.x;
+                if (e < lc) {
+                    load_code<M>(A.codes + (size_t)(lst + e) * M, w[u]);
+                    idv[u] = __ldg(A.ids + lst + e);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kUnroll; u++) {
+                const uint32_t e = e0 + u * NT + threadIdx.x;
+                if (e < lc) {
+                    float acc = cb;
+#pragma unroll
+                    for (int p = 0; p < M; p++) acc = __fadd_rn(acc, lut[p * K + code_at(w[u], p)]);
+                    if (acc < 0.f) acc = 0.f;
+                    offer(acc, idv[u]);
+                }
+            }
+            round_end();
+        }
+        __syncthreads();
+    }
+
     // Visit a list of cells: scan their entries (search) or record them
     // (traversal stage).  filt_d < 0: all cells; else only cells whose digit
     // filt_d is < filt_v.
@@ -383,6 +457,8 @@ struct Query {
             int oi = 0, oj = 0;
             uint32_t lst = 0;
             float cb = 0.f;
+            bool big = false;
+            if (threadIdx.x == 0) S.nbig = 0;
             if (c < n) {
                 int4 e = list[c];
                 bool pass = filt_d < 0 || digit(filt_d, e) < filt_v;
@@ -405,6 +481,7 @@ struct Query {
                         float s = __fadd_rn(__ldg(d1 + oi), __ldg(d2 + oj));
                         float t0 = __fsub_rn(S.qnorm, __fmul_rn(2.f, s));
                         cb = __fadd_rn(__fadd_rn(t0, __ldg(A.cn1 + oi)), __ldg(A.cn2 + oj));
+                        big = lc >= (uint32_t)kLutMin;
                     }
                 }
             }
@@ -412,12 +489,14 @@ struct Query {
                 continue;
             } else {
                 uint32_t E;
-                uint32_t ex = block_excl_scan(S, lc, &E);
+                uint32_t ex = block_excl_scan(S, big ? 0u : lc, &E);
                 S.cpre[threadIdx.x] = ex;
                 S.coi[threadIdx.x] = oi;
                 S.coj[threadIdx.x] = oj;
                 S.cstart[threadIdx.x] = lst;
                 S.cbase[threadIdx.x] = cb;
+                S.ccnt[threadIdx.x] = lc;
+                if (big) S.bigs[atomicAdd(&S.nbig, 1u)] = (uint16_t)threadIdx.x;
                 __syncthreads();
                 ncand += E;
                 for (uint32_t e0 = 0; e0 < E; e0 += NT * kUnroll) {
@@ -450,14 +529,17 @@ struct Query {
                             dist = dist_fbpq<M>(A, tab, S.coi[lo], S.coj[lo], S.cbase[lo], w[u]);
                         else
                             dist = dist_recon<ENGINE, M>(A, tab, S.coi[lo], S.coj[lo], w[u]);
-                        const unsigned long long kk = ((unsigned long long)canon_bits(dist) << 32) | idv[u];
-                        if (kk < S.thr) {
-                            uint32_t pos = atomicAdd(&S.ntk, 1u);
-                            S.tk[pos] = kk;
-                        }
+                        offer(dist, idv[u]);
                     }
-                    __syncthreads();
-                    if (S.ntk > (uint32_t)(kTopkBuf - NT * kUnroll)) topk_compact(S, A.k);
+                    round_end();
+                }
+                if constexpr (ENGINE == BPQ_ENGINE_FBPQ) {
+                    const uint32_t nb = S.nbig;
+                    for (uint32_t x = 0; x < nb; x++) {
+                        const int t = S.bigs[x];
+                        ncand += S.ccnt[t];
+                        scan_cell_lut(S.coi[t], S.coj[t], S.cstart[t], S.ccnt[t], S.cbase[t]);
+                    }
                 }
                 __syncthreads();
             }
@@ -465,41 +547,53 @@ struct Query {
         if constexpr (ENGINE == ENGINE_TRAVERSE) __syncthreads();
     }
 
-    // Cells with key <= tau (block-uniform result).  Row a's count is found
-    // by galloping from its current boundary rowB[a] (all cells left of it
-    // are already known to be <= tau); rowNew (optional) records it.
-    __device__ unsigned long long count_le(double tau, const int32_t *rowB, int32_t *rowNew) {
+    // first x in [lo, T) with base + k(x) > tau, galloping from lo (every x
+    // below lo is already known to satisfy base + k(x) <= tau)
+    template <bool ALONG_ROW>
+    __device__ __forceinline__ int gallop(double base, int lo, double tau) const {
+        auto kk = [&](int x) { return ALONG_ROW ? k2(x) : k1(x); };
+        if (lo >= T || !(base + kk(lo) <= tau)) return lo;
+        int p = lo, step = 1, hi = T;
+        for (;;) {
+            const int q = p + step;
+            if (q >= T) break;
+            if (base + kk(q) <= tau) {
+                p = q;
+                step <<= 1;
+            } else {
+                hi = q;
+                break;
+            }
+        }
+        int l2 = p + 1, h2 = hi;
+        while (l2 < h2) {
+            const int mid = (l2 + h2) >> 1;
+            if (base + kk(mid) <= tau) l2 = mid + 1; else h2 = mid;
+        }
+        return l2;
+    }
+
+    __device__ __forceinline__ int row_lo(const int32_t *rowB, int RA, int a) const { return a < RA ? rowB[a] : a; }
+    __device__ __forceinline__ int col_lo(const int32_t *colB, int CA, int b) const { return b < CA ? colB[b] : b + 1; }
+
+    // Cells with key <= tau (block-uniform result); rowNew/colNew (optional)
+    // receive the new boundaries of the active lines.
+    __device__ unsigned long long count_le(double tau, const int32_t *rowB, int RA, const int32_t *colB,
+                                           int CA, int32_t *rowNew, int32_t *colNew) {
         unsigned long long cnt = 0;
-        const double k0 = k2(0);
         for (int a = threadIdx.x; a < T; a += NT) {
             const double ka = k1(a);
-            if (!(ka + k0 <= tau)) break;
-            int lo = rowB[a];
-            int B;
-            if (lo >= T || !(ka + k2(lo) <= tau)) {
-                B = lo;
-            } else {
-                int p = lo, step = 1, hi = T;  // key(a, p) <= tau
-                for (;;) {
-                    int q = p + step;
-                    if (q >= T) break;
-                    if (ka + k2(q) <= tau) {
-                        p = q;
-                        step <<= 1;
-                    } else {
-                        hi = q;
-                        break;
-                    }
-                }
-                int l2 = p + 1, h2 = hi;  // first index in (p, hi] with key > tau
-                while (l2 < h2) {
-                    int mid = (l2 + h2) >> 1;
-                    if (ka + k2(mid) <= tau) l2 = mid + 1; else h2 = mid;
-                }
-                B = l2;
-            }
-            cnt += (unsigned)B;
+            if (!(ka + k2(a) <= tau)) break;
+            const int B = gallop<true>(ka, row_lo(rowB, RA, a), tau);
+            cnt += (unsigned)(B - a);
             if (rowNew) rowNew[a] = B;
+        }
+        for (int b = threadIdx.x; b + 1 < T; b += NT) {
+            const double kb = k2(b);
+            if (!(k1(b + 1) + kb <= tau)) break;
+            const int Av = gallop<false>(kb, col_lo(colB, CA, b), tau);
+            cnt += (unsigned)(Av - (b + 1));
+            if (colNew) colNew[b] = Av;
         }
         return block_sum_u64(S, cnt);
     }
@@ -590,64 +684,85 @@ struct Query {
         }
     }
 
-    // Enumerate the band: compacted rows r = 0..nrows-1 cover columns
-    // [recAB.lo16, recB1) of row recAB.hi16; each thread takes a contiguous
-    // run of the flattened band and keeps kEnumBatch cell-table reads in
-    // flight.  Non-empty cells are appended to the list.  Returns the band's
-    // global entry count.
-    __device__ unsigned long long enumerate_band(const uint32_t *recAB, const uint32_t *recB1,
-                                                 const uint32_t *recPre, int nrows, uint32_t sband,
-                                                 int4 *list) {
+    // Enumerate the band.  Segment r (seg[r] = {kind | sparse | line index,
+    // lo | hi << 16, work prefix, list base}, segLine[r] = codeword) covers
+    // cells [lo, hi) of one row (kind 0) or column (kind 1).  A dense
+    // segment has one work unit per cell; a sparse one has one per populated
+    // cell of its codeword's line, filtered by the cell's sorted position.
+    // Each thread takes a contiguous run of work units with kEnumBatch
+    // cell-table reads in flight.  Returns the band's global entry count.
+    __device__ unsigned long long enumerate_band(const uint4 *seg, const uint32_t *segLine, int nseg,
+                                                 uint32_t swork, int4 *list) {
         unsigned long long wb = 0;
-        const uint32_t per = (sband + NT - 1) / NT;
+        const uint32_t per = (swork + NT - 1) / NT;
         uint32_t f = threadIdx.x * per;
-        const uint32_t f1 = min(sband, f + per);
+        const uint32_t f1 = min(swork, f + per);
         if (f < f1) {
-            int lo = 0, hi = nrows;  // largest r with recPre[r] <= f
+            int lo = 0, hi = nseg;  // largest r with pre <= f
             while (hi - lo > 1) {
                 int mid = (lo + hi) >> 1;
-                if (recPre[mid] <= f) lo = mid; else hi = mid;
+                if (seg[mid].z <= f) lo = mid; else hi = mid;
             }
             int r = lo;
-            uint32_t ab = recAB[r];
-            int a = (int)(ab >> 16);
-            int b = (int)(ab & 0xFFFF) + (int)(f - recPre[r]);
-            int bend = (int)recB1[r];
+            uint4 sg = seg[r];
+            uint32_t line = segLine[r];
+            uint32_t u = f - sg.z;
+            uint32_t nxt = (r + 1 < nseg) ? seg[r + 1].z : swork;
             while (f < f1) {
                 int ca[kEnumBatch], cbv[kEnumBatch];
-                int na = 0;
+                unsigned long long lin[kEnumBatch];
+                bool ok[kEnumBatch];
 #pragma unroll
                 for (int x = 0; x < kEnumBatch; x++) {
+                    ok[x] = false;
                     if (f < f1) {
-                        if (b >= bend) {
+                        if (f >= nxt) {
                             r++;
-                            ab = recAB[r];
-                            a = (int)(ab >> 16);
-                            b = (int)(ab & 0xFFFF);
-                            bend = (int)recB1[r];
+                            sg = seg[r];
+                            line = segLine[r];
+                            u = 0;
+                            nxt = (r + 1 < nseg) ? seg[r + 1].z : swork;
                         }
-                        ca[x] = a;
-                        cbv[x] = b;
-                        b++;
+                        const bool col = (sg.x >> 31) != 0, sparse = ((sg.x >> 30) & 1) != 0;
+                        const int idx = (int)(sg.x & 0xFFFF);
+                        const int slo = (int)(sg.y & 0xFFFF), shi = (int)(sg.y >> 16);
+                        if (!sparse) {
+                            const int v = slo + (int)u;
+                            ca[x] = col ? v : idx;
+                            cbv[x] = col ? idx : v;
+                            lin[x] = col ? (unsigned long long)__ldg(o1 + v) * T + line
+                                         : (unsigned long long)line * T + (unsigned)__ldg(o2 + v);
+                            ok[x] = true;
+                        } else if (!col) {
+                            const uint32_t j = A.rowcols[sg.w + u];
+                            const int b = __ldg(p2 + j);
+                            ca[x] = idx;
+                            cbv[x] = b;
+                            lin[x] = (unsigned long long)line * T + j;
+                            ok[x] = b >= slo && b < shi;
+                        } else {
+                            const uint32_t i = A.colrows[sg.w + u];
+                            const int a = __ldg(p1 + i);
+                            ca[x] = a;
+                            cbv[x] = idx;
+                            lin[x] = (unsigned long long)i * T + line;
+                            ok[x] = a >= slo && a < shi;
+                        }
+                        u++;
                         f++;
-                        na = x + 1;
                     }
                 }
-                unsigned long long lin[kEnumBatch];
                 OffT g0[kEnumBatch], g1[kEnumBatch];
 #pragma unroll
-                for (int x = 0; x < kEnumBatch; x++)
-                    if (x < na) lin[x] = lin_of(ca[x], cbv[x]);
-#pragma unroll
                 for (int x = 0; x < kEnumBatch; x++) {
-                    if (x < na) {
+                    if (ok[x]) {
                         g0[x] = __ldg(A.goff + lin[x]);
                         g1[x] = __ldg(A.goff + lin[x] + 1);
                     }
                 }
 #pragma unroll
                 for (int x = 0; x < kEnumBatch; x++) {
-                    if (x < na && g1[x] > g0[x]) {
+                    if (ok[x] && g1[x] > g0[x]) {
                         uint32_t lst, lcn;
                         if (A.sharded) {
                             OffT l0 = __ldg(A.loff + lin[x]), l1 = __ldg(A.loff + lin[x] + 1);
@@ -671,14 +786,14 @@ struct Query {
     __device__ void run() {
         char *scr = A.scratch + (size_t)blockIdx.x * A.stride;
         int32_t *rowB = reinterpret_cast<int32_t *>(scr);
-        int32_t *rowNew = rowB + T;
-        uint32_t *recAB = reinterpret_cast<uint32_t *>(rowNew + T);
-        uint32_t *recB1 = recAB + T;
-        uint32_t *recPre = recB1 + T;
-        int4 *listA = reinterpret_cast<int4 *>(scr + (((size_t)5 * T * 4 + 15) & ~(size_t)15));
+        int32_t *colB = rowB + T;
+        int32_t *rowNew = colB + T;
+        int32_t *colNew = rowNew + T;
+        uint32_t *segLine = reinterpret_cast<uint32_t *>(colNew + T);
+        uint4 *seg = reinterpret_cast<uint4 *>(scr + (((size_t)6 * T * 4 + 15) & ~(size_t)15));
+        int4 *listA = reinterpret_cast<int4 *>(seg + 2 * T);
         int4 *listB = listA + kBandCap;
 
-        for (int a = threadIdx.x; a < T; a += NT) rowB[a] = 0;
         if (threadIdx.x == 0) {
             S.ntk = 0;
             S.thr = ~0ull;
@@ -687,9 +802,11 @@ struct Query {
         __syncthreads();
         if (A.n_global == 0) return;
 
+        const bool lists = A.rowptr != nullptr;
         const unsigned long long Tall = (unsigned long long)T * T;
         const unsigned long long L = (unsigned long long)A.L;
         unsigned long long W = 0, Cprev = 0;
+        int RA = 0, CA = 0;  // lines whose boundary arrays are initialised
         double tauLo = -1.0;
         const double maxKey = key(T - 1, T - 1);
         const double k00 = key(0, 0);
@@ -728,7 +845,7 @@ struct Query {
                         mid = lo + 0.5 * (hi - lo);
                         if (!(mid > lo && mid < hi)) break;
                     }
-                    unsigned long long cm = count_le(mid, rowB, nullptr);
+                    unsigned long long cm = count_le(mid, rowB, RA, colB, CA, nullptr, nullptr);
                     double band = (double)(cm - Cprev);
                     if (band > target) {
                         hi = mid;
@@ -759,49 +876,88 @@ struct Query {
                     return;
                 }
             }
-            // rows touched by this band and their new bounds
-            count_le(tauHi, rowB, rowNew);
+            // new line boundaries at tauHi and the active line counts
+            count_le(tauHi, rowB, RA, colB, CA, rowNew, colNew);
             if (threadIdx.x == 0) {
-                int lo = 0, hi = T;  // active rows: #{a : key(a,0) <= tauHi}
-                const double k0 = k2(0);
+                int lo = 0, hi = T;  // rows: #{a : key(a, a) <= tauHi}
                 while (lo < hi) {
                     int mid = (lo + hi) >> 1;
-                    if (k1(mid) + k0 <= tauHi) lo = mid + 1; else hi = mid;
+                    if (k1(mid) + k2(mid) <= tauHi) lo = mid + 1; else hi = mid;
                 }
                 S.arows = lo;
+                lo = 0;
+                hi = T - 1;  // columns: #{b < T-1 : key(b+1, b) <= tauHi}
+                while (lo < hi) {
+                    int mid = (lo + hi) >> 1;
+                    if (k1(mid + 1) + k2(mid) <= tauHi) lo = mid + 1; else hi = mid;
+                }
+                S.acols = lo;
             }
             __syncthreads();
-            const int arows = S.arows;
-            // compact the band's non-empty rows: (a, first column, end column,
-            // flattened prefix) so the enumeration never walks empty rows
-            uint32_t run = 0, nrows = 0;
-            for (int base = 0; base < arows; base += NT) {
-                const int a = base + threadIdx.x;
-                const int b0 = a < arows ? rowB[a] : 0;
-                const int b1 = a < arows ? rowNew[a] : 0;
-                const uint32_t len = (uint32_t)(b1 - b0);
-                uint32_t tot, totr;
-                const uint32_t ex = block_excl_scan(S, len, &tot);
-                const uint32_t exr = block_excl_scan(S, len > 0 ? 1u : 0u, &totr);
-                if (len > 0) {
-                    recAB[nrows + exr] = ((uint32_t)a << 16) | (uint32_t)b0;
-                    recB1[nrows + exr] = (uint32_t)b1;
-                    recPre[nrows + exr] = run + ex;
+            const int nR = S.arows, nC = S.acols;
+            // compact the band's non-empty segments with their work counts
+            uint32_t swork = 0, nseg = 0;
+            for (int base = 0; base < nR + nC; base += NT) {
+                const int v = base + threadIdx.x;
+                uint32_t len = 0, work = 0, lo = 0, hi = 0, ln = 0, lb = 0, hdr = 0;
+                bool sparse = false;
+                if (v < nR) {
+                    lo = (uint32_t)row_lo(rowB, RA, v);
+                    hi = (uint32_t)rowNew[v];
+                    len = hi - lo;
+                    if (len) {
+                        ln = (uint32_t)__ldg(o1 + v);
+                        if (lists) {
+                            const uint32_t p0 = __ldg(A.rowptr + ln), pe = __ldg(A.rowptr + ln + 1);
+                            sparse = pe - p0 < len;
+                            lb = p0;
+                            work = sparse ? pe - p0 : len;
+                        } else {
+                            work = len;
+                        }
+                        hdr = (sparse ? (1u << 30) : 0u) | (uint32_t)v;
+                    }
+                } else if (v < nR + nC) {
+                    const int b = v - nR;
+                    lo = (uint32_t)col_lo(colB, CA, b);
+                    hi = (uint32_t)colNew[b];
+                    len = hi - lo;
+                    if (len) {
+                        ln = (uint32_t)__ldg(o2 + b);
+                        if (lists) {
+                            const uint32_t p0 = __ldg(A.colptr + ln), pe = __ldg(A.colptr + ln + 1);
+                            sparse = pe - p0 < len;
+                            lb = p0;
+                            work = sparse ? pe - p0 : len;
+                        } else {
+                            work = len;
+                        }
+                        hdr = (1u << 31) | (sparse ? (1u << 30) : 0u) | (uint32_t)b;
+                    }
                 }
-                run += tot;
-                nrows += totr;
+                uint32_t tot, totr;
+                const uint32_t ex = block_excl_scan(S, work, &tot);
+                const uint32_t exr = block_excl_scan(S, work > 0 ? 1u : 0u, &totr);
+                if (work > 0) {
+                    seg[nseg + exr] = make_uint4(hdr, lo | (hi << 16), swork + ex, lb);
+                    segLine[nseg + exr] = ln;
+                }
+                swork += tot;
+                nseg += totr;
             }
-            const uint32_t sband = run;
             if (threadIdx.x == 0) S.nlist = 0;
             __syncthreads();
-            const unsigned long long wb = enumerate_band(recAB, recB1, recPre, (int)nrows, sband, listA);
+            const unsigned long long wb = enumerate_band(seg, segLine, (int)nseg, swork, listA);
             const int n = (int)S.nlist;
             if (W + wb < L) {
                 emit(listA, n, -1, 0);
                 W += wb;
                 Cprev = cHi;
-                for (int a = threadIdx.x; a < arows; a += NT) rowB[a] = rowNew[a];
+                for (int a = threadIdx.x; a < nR; a += NT) rowB[a] = rowNew[a];
+                for (int b = threadIdx.x; b < nC; b += NT) colB[b] = colNew[b];
                 __syncthreads();
+                RA = max(RA, nR);
+                CA = max(CA, nC);
                 tauLo = tauHi;
                 if (cHi == Tall) {
                     popped = Tall;
@@ -813,7 +969,8 @@ struct Query {
                 final_select(listA, listB, n, L - W);
                 if (A.out_popped) {
                     __syncthreads();
-                    popped = count_le(__longlong_as_double((long long)S.cut_key), rowB, nullptr);
+                    popped = count_le(__longlong_as_double((long long)S.cut_key), rowB, RA, colB, CA,
+                                      nullptr, nullptr);
                 }
                 break;
             }
@@ -868,6 +1025,7 @@ __global__ void __launch_bounds__(NT, BPQ_MINB) search_kernel(Args<KT, OffT> A) 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem &S = *reinterpret_cast<Smem *>(smem_raw);
     float *tab = reinterpret_cast<float *>(smem_raw + sizeof(Smem));
+    float *lut = tab + (ENGINE == BPQ_ENGINE_FBPQ ? M * A.K : 0);
     KT *s1s = reinterpret_cast<KT *>(tab + A.tab_floats);
     KT *s2s = s1s + A.sr_smem;
     for (;;) {
@@ -909,7 +1067,7 @@ __global__ void __launch_bounds__(NT, BPQ_MINB) search_kernel(Args<KT, OffT> A) 
             }
         }
         __syncthreads();
-        Query<ENGINE, M, KT, OffT> Q(A, S, qi, tab, s1s, s2s);
+        Query<ENGINE, M, KT, OffT> Q(A, S, qi, tab, lut, s1s, s2s);
         Q.run();
         Q.finish();
         __syncthreads();
@@ -954,9 +1112,9 @@ int launch_one(const Index &ix, const float *queries, int64_t q0, int64_t nq, in
                int32_t k, const SearchWorkspace &ws, float *out_dist, uint32_t *out_ids,
                int32_t *out_count, int64_t *out_ncand, int64_t *out_popped, cudaStream_t stream) {
     Args<float, uint32_t> A{};
-    A.tab_floats = ENGINE == BPQ_ENGINE_FBPQ ? M * ix.K : ix.D;
+    A.tab_floats = ENGINE == BPQ_ENGINE_FBPQ ? 2 * M * ix.K : ix.D;  // fold + per-cell LUT
     A.tab_floats = (A.tab_floats + 3) & ~3;
-    A.sr_smem = ix.T < kSrSmem ? ix.T : kSrSmem;
+    A.sr_smem = 0;  // sorted keys are read through L1: only active lines are probed
     const size_t smem = dyn_smem_bytes(A.tab_floats, A.sr_smem, sizeof(float));
     int n_cta = 0;
     int rc = configure<ENGINE, M, float, uint32_t>(smem, &n_cta);
@@ -993,6 +1151,12 @@ int launch_one(const Index &ix, const float *queries, int64_t q0, int64_t nq, in
     A.sr2 = ws.sr2;
     A.ord1 = ws.ord1;
     A.ord2 = ws.ord2;
+    A.pos1 = ws.pos1;
+    A.pos2 = ws.pos2;
+    A.rowptr = ix.rowptr;
+    A.colptr = ix.colptr;
+    A.rowcols = ix.rowcols;
+    A.colrows = ix.colrows;
     A.L = budget;
     A.k = k;
     A.out_d = out_dist;

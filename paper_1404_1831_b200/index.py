@@ -105,7 +105,7 @@ class DeviceIndex:
     streams as long as each uses its own workspace (``workspace=``)."""
 
     def __init__(self, *, c1, c2, offsets, ids, codes, books=None, tables=None, bank1=None,
-                 bank2=None, global_offsets=None, device=None, num_entries_global=None):
+                 bank2=None, global_offsets=None, device=None, num_entries_global=None, cell_lists="auto"):
         import torch
 
         self.device = torch.device(device if device is not None else "cuda")
@@ -170,9 +170,38 @@ class DeviceIndex:
             self.cross2 = _f32(_table_attr(tables, 4), dev)
         self.bank1 = _f32(bank1, dev)
         self.bank2 = _f32(bank2, dev)
+        self._build_cell_lists(cell_lists)
         self._handle = None
         self._ws = None
         self._create()
+
+    # ------------------------------------------------------ populated cells
+    def _build_cell_lists(self, mode):
+        """Row/column lists of the traversal table's populated cells
+        (bpq_build_cell_lists).  'auto' builds them when under half of the
+        cells are populated -- then the traversal enumerates sparse band
+        segments through them instead of reading every cell's offsets."""
+        import torch
+
+        self.row_ptr = self.col_ptr = self.row_cols = self.col_rows = None
+        if mode is False or mode == "off":
+            return
+        table = self.global_offsets if self.global_offsets is not None else self.offsets
+        t = self.t
+        populated = int(((table[1:].long() & 0xFFFFFFFF) != (table[:-1].long() & 0xFFFFFFFF)).sum().item())
+        if mode == "auto" and populated * 2 > t * t:
+            return
+        dev = self.device
+        self.row_ptr = torch.empty(t + 1, dtype=torch.int32, device=dev)
+        self.col_ptr = torch.empty(t + 1, dtype=torch.int32, device=dev)
+        self.row_cols = torch.empty(max(populated, 1), dtype=torch.int16, device=dev)
+        self.col_rows = torch.empty(max(populated, 1), dtype=torch.int16, device=dev)
+        lib = _lib.load()
+        ws = torch.empty(int(lib.bpq_cell_lists_workspace_size(t)), dtype=torch.uint8, device=dev)
+        _lib.check(lib.bpq_build_cell_lists(_lib.ptr(table), t, _lib.ptr(self.row_ptr), _lib.ptr(self.row_cols),
+                                            _lib.ptr(self.col_ptr), _lib.ptr(self.col_rows), _lib.ptr(ws),
+                                            ws.numel(), _lib.stream_ptr()), "build_cell_lists")
+        self.populated_cells = populated
 
     # ------------------------------------------------------------- C handle
     def _create(self):
@@ -189,6 +218,8 @@ class DeviceIndex:
         d.fine_books, d.fine_norms = _lib.ptr(self.books), _lib.ptr(self.fine_norms)
         d.cross1, d.cross2 = _lib.ptr(self.cross1), _lib.ptr(self.cross2)
         d.bank1, d.bank2 = _lib.ptr(self.bank1), _lib.ptr(self.bank2)
+        d.row_ptr, d.col_ptr = _lib.ptr(self.row_ptr), _lib.ptr(self.col_ptr)
+        d.row_cols, d.col_rows = _lib.ptr(self.row_cols), _lib.ptr(self.col_rows)
         h = ctypes.c_void_p()
         _lib.check(lib.bpq_index_create(ctypes.byref(d), 0, ctypes.byref(h)), "bpq_index_create")
         self._handle = h

@@ -157,6 +157,50 @@ def test_search_vs_oracle_small_synthetic(torch_cuda, oracle):
             check_topk(d, i, c, wd, wi, wc, _qn(q), min_exact_frac=0.95 if k <= 50 else 0.5)
 
 
+@pytest.mark.parametrize("engine", ["fbpq", "baseline"])
+def test_cell_lists_do_not_change_results(c0, torch_cuda, engine):
+    """Sparse band enumeration (populated-cell lists) is an exact
+    re-implementation of the dense one: identical outputs."""
+    from paper_1404_1831_b200 import DeviceIndex
+
+    tables = (c0["cn1"], c0["cn2"], c0["fine_norms"], c0["cross1"], c0["cross2"])
+    kw = dict(c1=c0["c1"], c2=c0["c2"], offsets=c0["offsets"], ids=c0["ids"], codes=c0["codes"],
+              books=c0["books"], tables=tables)
+    dense = DeviceIndex(cell_lists=False, **kw)
+    sparse = DeviceIndex(cell_lists=True, **kw)
+    assert sparse.row_ptr is not None and dense.row_ptr is None
+    q = c0["queries"][:300].astype(np.float32)
+    for L, k in ((10_000, 100), (1_000, 10), (1, 1), (200_000, 5)):
+        a = dense.search(q, L, k, engine, ncand=True)
+        b = sparse.search(q, L, k, engine, ncand=True)
+        for x, y in zip(a.numpy(), b.numpy()):
+            np.testing.assert_array_equal(x, y)
+        np.testing.assert_array_equal(a.ncand.cpu().numpy(), b.ncand.cpu().numpy())
+
+
+def test_sparse_table_vs_oracle(torch_cuda, oracle):
+    """A mostly-empty cell table (clustered data, large T) with lists on."""
+    from paper_1404_1831_b200 import DeviceIndex
+
+    rng = np.random.default_rng(3)
+    t, dim, m, kk, n = 200, 32, 4, 32, 20_000
+    cent = rng.normal(scale=5.0, size=(60, dim)).astype(np.float32)
+    base = (cent[rng.integers(0, 60, n)] + rng.normal(size=(n, dim))).astype(np.float32)
+    c1 = base[rng.choice(n, t, replace=False), : dim // 2].copy()
+    c2 = base[rng.choice(n, t, replace=False), dim // 2 :].copy()
+    books = rng.normal(scale=0.5, size=(m, kk, dim // m)).astype(np.float32)
+    off, ids, codes = oracle.build_index(base, c1, c2, books)
+    assert np.count_nonzero(np.diff(off)) < t * t // 4
+    idx = oracle.Index(c1, c2, off, ids, codes, books=books)
+    dix = DeviceIndex(c1=c1, c2=c2, offsets=off, ids=ids, codes=codes, books=books, tables=idx.tables)
+    assert dix.row_ptr is not None
+    q = (cent[rng.integers(0, 60, 64)] + rng.normal(size=(64, dim))).astype(np.float32)
+    for L, k in ((1, 1), (100, 10), (2000, 100), (50_000, 20)):
+        wd, wi, wc, _ = oracle.search_batch_numpy(idx, "fbpq", q, L, k)
+        d, i, c = dix.search(q, L, k, "fbpq").numpy()
+        check_topk(d, i, c, wd, wi, wc, _qn(q), min_exact_frac=0.9)
+
+
 def test_empty_index_returns_nothing(torch_cuda):
     from paper_1404_1831_b200 import DeviceIndex
 
