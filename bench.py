@@ -207,6 +207,8 @@ def main():
     ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--nq", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--phase-profile", action="store_true",
+                    help="print per-phase cycle shares of the fused kernel (needs BPQ_LIB=...libbpq_b200_prof.so)")
     args = ap.parse_args()
 
     import torch
@@ -288,6 +290,19 @@ def main():
         raise RuntimeError(f"{int((counts < 0).sum())} queries hit the tie-plateau limit")
     ncand = int(out.ncand.sum().item())
     npop = int(popped.sum().item())
+    if args.phase_profile:
+        from paper_1404_1831_b200 import _lib
+
+        ctr = torch.zeros(16, dtype=torch.int64, device=device)
+        on = _lib.load().bpq_debug_set_phase_buffer(_lib.ptr(ctr))
+        dix.search(q, L, k, engine, out=out, workspace=ws)
+        torch.cuda.synchronize()
+        _lib.load().bpq_debug_set_phase_buffer(None)
+        names = ["prologue", "tau_search", "band_bounds", "enumerate", "scan", "lut_scan", "topk_compact",
+                 "final_select", "finish", "idle"]
+        c = ctr.cpu().numpy()[:10].astype(float)
+        log(json.dumps({"phase_profile_compiled": bool(on),
+                        "phase_share": {n: round(float(v / max(c.sum(), 1)), 4) for n, v in zip(names, c)}}))
     for _ in range(args.warmup):
         dix.search(q, L, k, engine, out=out, workspace=ws)
     torch.cuda.synchronize()

@@ -173,6 +173,13 @@ int bpq_build_cell_lists(const uint32_t *offsets, int32_t t, uint32_t *row_ptr, 
                          uint32_t *col_ptr, uint16_t *col_rows, void *workspace,
                          size_t workspace_bytes, void *stream);
 
+/* Diagnostics: device buffer of 10 u64 cycle counters that the fused
+ * search kernel fills per phase (prologue, tau search, band bounds,
+ * enumeration, scan, LUT scan, top-k compaction, final select, finish,
+ * idle) when the library was built with -DBPQ_PHASE_PROF; returns 1 if
+ * compiled in, else 0 (and the buffer is never written). */
+int bpq_debug_set_phase_buffer(unsigned long long *dev_counters);
+
 /* Merge per-shard top-k lists [g, nq, k] into [nq, k] by (dist, id). */
 int bpq_merge_topk(const float *dists, const uint32_t *ids, const int32_t *counts, int32_t g,
                    int64_t nq, int32_t k, float *out_dist, uint32_t *out_ids,

@@ -75,6 +75,7 @@ SIGNATURES = {
     "bpq_pack_cells": (ctypes.c_int, [P, P, I64, I32, ctypes.c_uint32, P, I32, P, P, P, P, SZ, P]),
     "bpq_cell_lists_workspace_size": (SZ, [I32]),
     "bpq_build_cell_lists": (ctypes.c_int, [P, I32, P, P, P, P, P, SZ, P]),
+    "bpq_debug_set_phase_buffer": (ctypes.c_int, [P]),
     "bpq_merge_topk": (ctypes.c_int, [P, P, P, I32, I64, I32, P, P, P, P]),
 }
 

@@ -5,6 +5,9 @@
 #include "search_impl.cuh"
 
 namespace bpq {
+void set_prof_buffer_e0(unsigned long long *);
+void set_prof_buffer_e1(unsigned long long *);
+void set_prof_buffer_e2(unsigned long long *);
 int launch_search_e0(const Index &, const float *, int64_t, int64_t, int64_t, int32_t, const SearchWorkspace &,
                      float *, uint32_t *, int32_t *, int64_t *, int64_t *, cudaStream_t);
 int launch_search_e1(const Index &, const float *, int64_t, int64_t, int64_t, int32_t, const SearchWorkspace &,
@@ -257,6 +260,20 @@ int launch_traverse_stage(const double *sr1, const double *sr2, const int32_t *o
 }
 
 }  // namespace bpq
+
+// ------------------------------------------------------- C ABI: diagnostics
+extern "C" int bpq_debug_set_phase_buffer(unsigned long long *dev_counters) {
+    // every translation unit keeps its own pointer; set all of them
+    bpq::g_prof_buffer = dev_counters;
+    bpq::set_prof_buffer_e0(dev_counters);
+    bpq::set_prof_buffer_e1(dev_counters);
+    bpq::set_prof_buffer_e2(dev_counters);
+#ifdef BPQ_PHASE_PROF
+    return 1;
+#else
+    return 0;
+#endif
+}
 
 // --------------------------------------------------------------- C ABI: scans
 using bpq::fail;

@@ -4,6 +4,8 @@
 
 namespace bpq {
 
+void set_prof_buffer_e0(unsigned long long *p) { g_prof_buffer = p; }
+
 int launch_search_e0(const Index &ix, const float *queries, int64_t q0, int64_t nq, int64_t budget,
                       int32_t k, const SearchWorkspace &ws, float *od, uint32_t *oi, int32_t *oc,
                       int64_t *on, int64_t *op, cudaStream_t s) {

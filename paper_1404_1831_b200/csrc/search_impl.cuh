@@ -80,11 +80,39 @@ struct __align__(16) Smem {
     uint32_t nlist;
     float qnorm;
     int sel_v;
-    int arows;
-    int acols;
+    int cnt_nr;
+    int cnt_nc;
     uint32_t nbig;
     int err;
+    int prof_ph;
+    long long prof_t;
+    // top-k compaction scratch (separate: compaction runs inside final_select)
+    int tsel_v;
+    uint32_t tcnt;
+    unsigned long long tsel_below;
+    unsigned long long tkey;
 };
+
+#ifdef BPQ_PHASE_PROF
+__device__ __forceinline__ int prof_switch(Smem &S, unsigned long long *acc, int ph) {
+    int prev = S.prof_ph;
+    __syncwarp();
+    if (threadIdx.x == 0 && acc) {
+        long long now = clock64();
+        atomicAdd(acc + S.prof_ph, (unsigned long long)(now - S.prof_t));
+        S.prof_t = now;
+        S.prof_ph = ph;
+    }
+    return prev;
+}
+#define PROF(ph) prof_switch(S, A.prof, (ph))
+#else
+#define PROF(ph) 0
+#endif
+
+// Optional per-phase cycle accounting (compile with -DBPQ_PHASE_PROF): thread 0
+// of each CTA attributes elapsed clock64 cycles to the current phase.
+enum Phase { PH_PROLOGUE, PH_TAU, PH_BOUNDS, PH_ENUM, PH_SCAN, PH_LUT, PH_COMPACT, PH_FINAL, PH_FINISH, PH_IDLE, PH_N };
 
 template <typename KT, typename OffT>
 struct Args {
@@ -122,6 +150,7 @@ struct Args {
     uint32_t *tv_lin;
     int64_t *tv_start, *tv_end;
     unsigned long long *tv_n;
+    unsigned long long *prof;  // [PH_N] cycle counters (phase-profiling builds)
 };
 
 // ---------------------------------------------------------------- block utils
@@ -317,17 +346,83 @@ __device__ __forceinline__ float dist_recon(const Args<KT, OffT> &A, const float
 }
 
 // ------------------------------------------------------------ top-k buffer
-__device__ __forceinline__ void topk_compact(Smem &S, int k) {
-    uint32_t n = S.ntk;
-    for (int i = threadIdx.x; i < kTopkBuf; i += NT)
-        if (i >= (int)n) S.tk[i] = ~0ull;
-    __syncthreads();
-    bitonic_sort_u64(S.tk, kTopkBuf);
-    if (threadIdx.x == 0) {
-        if ((int)n > k) {
-            S.ntk = k;
-            S.thr = S.tk[k - 1];
+// Keep the k smallest of the n > k buffered keys (keys are unique: the id
+// is in the low word).  An MSB-first radix select on the 64-bit keys finds
+// the k-th smallest in a few 256-bin histogram passes, then the survivors
+// are compacted to the front and the admission threshold becomes that key.
+__device__ void topk_compact(Smem &S, int k) {
+    const uint32_t n = S.ntk;
+    if ((int)n <= k) return;
+    unsigned long long prefix = 0, pmask = 0;
+    uint32_t rank = (uint32_t)k;  // 1-based rank of the wanted key among matches
+    for (int shift = 56; shift >= 0; shift -= 8) {
+        for (int i = threadIdx.x; i < 256; i += NT) S.hist_c[i] = 0;
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < n; i += NT) {
+            const unsigned long long key = S.tk[i];
+            if ((key & pmask) == prefix) atomicAdd(&S.hist_c[(key >> shift) & 0xFF], 1u);
         }
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            // warp scan over 256 bins (8 per lane)
+            const int lane = threadIdx.x;
+            uint32_t loc[8], sum = 0;
+#pragma unroll
+            for (int x = 0; x < 8; x++) {
+                loc[x] = S.hist_c[lane * 8 + x];
+                sum += loc[x];
+            }
+            uint32_t incl = sum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            uint32_t run = incl - sum;
+#pragma unroll
+            for (int x = 0; x < 8; x++) {
+                if (run < rank && run + loc[x] >= rank) {
+                    S.tsel_v = lane * 8 + x;
+                    S.tsel_below = run;
+                    S.tcnt = loc[x];
+                }
+                run += loc[x];
+            }
+        }
+        __syncthreads();
+        const unsigned long long d = (unsigned long long)S.tsel_v;
+        rank -= (uint32_t)S.tsel_below;
+        prefix |= d << shift;
+        pmask |= 0xFFull << shift;
+        if (S.tcnt == 1u) {
+            // a single key carries this prefix: it is the k-th smallest
+            for (uint32_t i = threadIdx.x; i < n; i += NT)
+                if ((S.tk[i] & pmask) == prefix) S.tkey = S.tk[i];
+            __syncthreads();
+            prefix = S.tkey;
+            break;
+        }
+        __syncthreads();
+    }
+    const unsigned long long kth = prefix;
+    // compact keys <= kth (exactly k of them) to the front
+    unsigned long long keep[kTopkBuf / NT];
+    int nk = 0;
+#pragma unroll
+    for (int x = 0; x < kTopkBuf / NT; x++) {
+        const uint32_t i = threadIdx.x + x * NT;
+        if (i < n && S.tk[i] <= kth) keep[nk++] = S.tk[i];
+    }
+    if (threadIdx.x == 0) S.tcnt = 0;
+    __syncthreads();
+    uint32_t base = nk ? atomicAdd(&S.tcnt, (uint32_t)nk) : 0;
+#pragma unroll
+    for (int x = 0; x < kTopkBuf / NT; x++)
+        if (x < nk) S.tk[base + x] = keep[x];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        S.ntk = (uint32_t)k;
+        S.thr = kth;
     }
     __syncthreads();
 }
@@ -404,13 +499,20 @@ struct Query {
 
     __device__ __forceinline__ void round_end() {
         __syncthreads();
-        if (S.ntk > (uint32_t)(kTopkBuf - NT * kUnroll)) topk_compact(S, A.k);
+        if (S.ntk > (uint32_t)(kTopkBuf - NT * kUnroll)) {
+            const int pv = PROF(PH_COMPACT);
+            topk_compact(S, A.k);
+            PROF(pv);
+            (void)pv;
+        }
     }
 
     // FBPQ, one large cell: LUT[p][c] = fold[p][c] + 2*cross[row][p][c] is
     // exactly the reference's per-part increment (numba_backend.py:236-240),
     // staged once so each entry costs M shared-memory lookups.
     __device__ void scan_cell_lut(int oi, int oj, uint32_t lst, uint32_t lc, float cb) {
+        const int pv = PROF(PH_LUT);
+        (void)pv;
         constexpr int M2 = M / 2;
         const int K = A.K;
         for (int idx = threadIdx.x; idx < M * K; idx += NT) {
@@ -445,12 +547,15 @@ struct Query {
             round_end();
         }
         __syncthreads();
+        PROF(pv);
     }
 
     // Visit a list of cells: scan their entries (search) or record them
     // (traversal stage).  filt_d < 0: all cells; else only cells whose digit
     // filt_d is < filt_v.
     __device__ void emit(const int4 *list, int n, int filt_d, int filt_v) {
+        const int pv = PROF(PH_SCAN);
+        (void)pv;
         for (int base = 0; base < n; base += NT) {
             int c = base + threadIdx.x;
             uint32_t lc = 0;
@@ -545,6 +650,7 @@ struct Query {
             }
         }
         if constexpr (ENGINE == ENGINE_TRAVERSE) __syncthreads();
+        PROF(pv);
     }
 
     // first x in [lo, T) with base + k(x) > tau, galloping from lo (every x
@@ -576,30 +682,87 @@ struct Query {
     __device__ __forceinline__ int row_lo(const int32_t *rowB, int RA, int a) const { return a < RA ? rowB[a] : a; }
     __device__ __forceinline__ int col_lo(const int32_t *colB, int CA, int b) const { return b < CA ? colB[b] : b + 1; }
 
+    // First x in [lo, hi) where the monotone predicate turns false (hi if
+    // never), found by the whole warp: one 32-wide galloping probe round,
+    // then 32-ary narrowing -- about log32(range) + 1 dependent loads.
+    template <class F>
+    __device__ __forceinline__ int warp_first_false(F pred, int lo, int hi) const {
+        const int lane = threadIdx.x & 31;
+        if (lo >= hi) return lo;
+        const long long p = (long long)lo + ((1ll << lane) - 1);
+        const unsigned m = __ballot_sync(0xffffffffu, p < hi && pred((int)p));
+        const int c = __popc(m);
+        if (c == 0) return lo;
+        int a = lo + (int)((1ll << (c - 1)) - 1);  // last true probe
+        int b = c < 31 ? (int)min((long long)hi, (long long)lo + (1ll << c) - 1) : hi;
+        while (b - a > 1) {
+            const int step = (b - a + 31) / 32;
+            const long long pp = (long long)a + (long long)(lane + 1) * step;
+            const unsigned mm = __ballot_sync(0xffffffffu, pp < b && pred((int)pp));
+            const int cc = __popc(mm);
+            const int na = a + cc * step;
+            b = (int)min((long long)b, (long long)a + (long long)(cc + 1) * step);
+            a = na;
+        }
+        return b;
+    }
+
     // Cells with key <= tau (block-uniform result); rowNew/colNew (optional)
-    // receive the new boundaries of the active lines.
+    // receive the new boundaries of the active lines and S.cnt_nr/cnt_nc the
+    // active line counts.  Few active lines (the common, thin staircase):
+    // one warp per line; many: one thread per line with a galloping search.
     __device__ unsigned long long count_le(double tau, const int32_t *rowB, int RA, const int32_t *colB,
                                            int CA, int32_t *rowNew, int32_t *colNew) {
-        unsigned long long cnt = 0;
-        for (int a = threadIdx.x; a < T; a += NT) {
-            const double ka = k1(a);
-            if (!(ka + k2(a) <= tau)) break;
-            const int B = gallop<true>(ka, row_lo(rowB, RA, a), tau);
-            cnt += (unsigned)(B - a);
-            if (rowNew) rowNew[a] = B;
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        if (warp == 0) {
+            const int nr = warp_first_false([&](int a) { return k1(a) + k2(a) <= tau; }, 0, T);
+            const int nc = warp_first_false([&](int b) { return k1(b + 1) + k2(b) <= tau; }, 0, T - 1);
+            if (lane == 0) {
+                S.cnt_nr = nr;
+                S.cnt_nc = nc;
+            }
         }
-        for (int b = threadIdx.x; b + 1 < T; b += NT) {
-            const double kb = k2(b);
-            if (!(k1(b + 1) + kb <= tau)) break;
-            const int Av = gallop<false>(kb, col_lo(colB, CA, b), tau);
-            cnt += (unsigned)(Av - (b + 1));
-            if (colNew) colNew[b] = Av;
+        __syncthreads();
+        const int nR = S.cnt_nr, nC = S.cnt_nc, nl = nR + nC;
+        unsigned long long cnt = 0;
+        if (nl <= 4 * NW) {
+            for (int line = warp; line < nl; line += NW) {
+                int B, start;
+                if (line < nR) {
+                    const int a = line;
+                    const double ka = k1(a);
+                    start = a;
+                    B = warp_first_false([&](int x) { return ka + k2(x) <= tau; }, row_lo(rowB, RA, a), T);
+                    if (rowNew && lane == 0) rowNew[a] = B;
+                } else {
+                    const int b = line - nR;
+                    const double kb = k2(b);
+                    start = b + 1;
+                    B = warp_first_false([&](int x) { return k1(x) + kb <= tau; }, col_lo(colB, CA, b), T);
+                    if (colNew && lane == 0) colNew[b] = B;
+                }
+                if (lane == 0) cnt += (unsigned)(B - start);
+            }
+        } else {
+            for (int a = threadIdx.x; a < nR; a += NT) {
+                const double ka = k1(a);
+                const int B = gallop<true>(ka, row_lo(rowB, RA, a), tau);
+                cnt += (unsigned)(B - a);
+                if (rowNew) rowNew[a] = B;
+            }
+            for (int b = threadIdx.x; b < nC; b += NT) {
+                const double kb = k2(b);
+                const int Av = gallop<false>(kb, col_lo(colB, CA, b), tau);
+                cnt += (unsigned)(Av - (b + 1));
+                if (colNew) colNew[b] = Av;
+            }
         }
         return block_sum_u64(S, cnt);
     }
 
     // exact cutoff inside the final band (weighted select, then smem sort)
     __device__ void final_select(int4 *cur, int4 *other, int n, unsigned long long need) {
+        PROF(PH_FINAL);
         for (int d = 0;; d++) {
             if (n <= kSortCap) {
                 int P2 = 1;
@@ -826,6 +989,7 @@ struct Query {
                 tauHi = hi;
                 cHi = chi;
                 const double want = (double)Cprev + target;
+                PROF(PH_TAU);
                 for (int it = 0; it < 200; it++) {
                     const double xlo = fmax(lo - k00, 0.0), xhi = hi - k00;
                     if (!(xhi > 0.0)) break;
@@ -877,24 +1041,9 @@ struct Query {
                 }
             }
             // new line boundaries at tauHi and the active line counts
+            PROF(PH_BOUNDS);
             count_le(tauHi, rowB, RA, colB, CA, rowNew, colNew);
-            if (threadIdx.x == 0) {
-                int lo = 0, hi = T;  // rows: #{a : key(a, a) <= tauHi}
-                while (lo < hi) {
-                    int mid = (lo + hi) >> 1;
-                    if (k1(mid) + k2(mid) <= tauHi) lo = mid + 1; else hi = mid;
-                }
-                S.arows = lo;
-                lo = 0;
-                hi = T - 1;  // columns: #{b < T-1 : key(b+1, b) <= tauHi}
-                while (lo < hi) {
-                    int mid = (lo + hi) >> 1;
-                    if (k1(mid + 1) + k2(mid) <= tauHi) lo = mid + 1; else hi = mid;
-                }
-                S.acols = lo;
-            }
-            __syncthreads();
-            const int nR = S.arows, nC = S.acols;
+            const int nR = S.cnt_nr, nC = S.cnt_nc;
             // compact the band's non-empty segments with their work counts
             uint32_t swork = 0, nseg = 0;
             for (int base = 0; base < nR + nC; base += NT) {
@@ -947,6 +1096,7 @@ struct Query {
             }
             if (threadIdx.x == 0) S.nlist = 0;
             __syncthreads();
+            PROF(PH_ENUM);
             const unsigned long long wb = enumerate_band(seg, segLine, (int)nseg, swork, listA);
             const int n = (int)S.nlist;
             if (W + wb < L) {
@@ -979,6 +1129,7 @@ struct Query {
 
     __device__ void finish() {
         if constexpr (ENGINE == ENGINE_TRAVERSE) return;
+        PROF(PH_FINISH);
         __syncthreads();
         const int k = A.k;
         const int64_t qo = A.q0 + qi;
@@ -994,6 +1145,7 @@ struct Query {
             }
             return;
         }
+        topk_compact(S, k);
         uint32_t n = S.ntk;
         int P2 = 1;
         while (P2 < (int)n) P2 <<= 1;
@@ -1028,11 +1180,21 @@ __global__ void __launch_bounds__(NT, BPQ_MINB) search_kernel(Args<KT, OffT> A) 
     float *lut = tab + (ENGINE == BPQ_ENGINE_FBPQ ? M * A.K : 0);
     KT *s1s = reinterpret_cast<KT *>(tab + A.tab_floats);
     KT *s2s = s1s + A.sr_smem;
+#ifdef BPQ_PHASE_PROF
+    if (threadIdx.x == 0) {
+        S.prof_ph = PH_IDLE;
+        S.prof_t = clock64();
+    }
+#endif
     for (;;) {
         if (threadIdx.x == 0) S.qidx = (int64_t)atomicAdd(A.counter, 1u);
         __syncthreads();
         const int64_t qi = S.qidx;
-        if (qi >= A.nq) return;
+        if (qi >= A.nq) {
+            PROF(PH_IDLE);
+            return;
+        }
+        PROF(PH_PROLOGUE);
         // stage the sorted half-distance prefixes
         {
             const KT *g1 = A.sr1 + qi * A.T, *g2 = A.sr2 + qi * A.T;
@@ -1073,6 +1235,8 @@ __global__ void __launch_bounds__(NT, BPQ_MINB) search_kernel(Args<KT, OffT> A) 
         __syncthreads();
     }
 }
+
+unsigned long long *g_prof_buffer = nullptr;
 
 size_t dyn_smem_bytes(int tab_floats, int sr_smem, size_t kt_size) {
     return sizeof(Smem) + (size_t)tab_floats * 4 + 2 * (size_t)sr_smem * kt_size;
@@ -1159,6 +1323,7 @@ int launch_one(const Index &ix, const float *queries, int64_t q0, int64_t nq, in
     A.colrows = ix.colrows;
     A.L = budget;
     A.k = k;
+    A.prof = g_prof_buffer;
     A.out_d = out_dist;
     A.out_ids = out_ids;
     A.out_count = out_count;
