@@ -31,6 +31,7 @@ constexpr int kSearchThreads = 256;     // threads per CTA (one CTA per query at
 constexpr int kTopkBuf = 2048;          // per-CTA top-k candidate buffer (u64 keys)
 constexpr int kMaxK = kTopkBuf - 4 * kSearchThreads;  // largest k the engine accepts
 constexpr int kSortCap = 512;           // final-band cells sorted in shared memory
+constexpr int kMultiLines = 8;          // lines a warp evaluates per threshold in a multi-probe round
 constexpr int kLutMin = 96;             // cells with >= this many entries are scanned via a smem LUT
 constexpr int kBandCap = 32768;         // max cells enumerated per band
 constexpr int kMaxDim = 1024;           // queries staged in shared memory

@@ -161,7 +161,7 @@ TravLayout trav_layout(int64_t t, int64_t budget, int64_t total) {
 
 size_t search_cta_scratch_bytes(int32_t T) {
     return (((size_t)6 * T * 4 + 15) & ~(size_t)15) + (size_t)2 * T * sizeof(uint4) +
-           (size_t)2 * kBandCap * sizeof(int4);
+           (size_t)4 * kBandCap * sizeof(int4);
 }
 
 

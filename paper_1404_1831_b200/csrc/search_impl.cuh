@@ -82,6 +82,8 @@ struct __align__(16) Smem {
     int sel_v;
     int cnt_nr;
     int cnt_nc;
+    double mtau[NW];
+    unsigned long long mcnt[NW];
     uint32_t nbig;
     int err;
     int prof_ph;
@@ -116,7 +118,7 @@ enum Phase { PH_PROLOGUE, PH_TAU, PH_BOUNDS, PH_ENUM, PH_SCAN, PH_LUT, PH_COMPAC
 
 template <typename KT, typename OffT>
 struct Args {
-    int T, D, dh, ds, K;
+    int T, D, dh, ds, K, M;
     const float *c1, *c2, *cn1, *cn2;
     const OffT *loff, *goff;
     bool sharded;
@@ -253,24 +255,26 @@ __device__ __forceinline__ uint32_t canon_bits(float d) {
 }
 
 // ------------------------------------------------------------ code loading
-template <int M>
-__device__ __forceinline__ void load_code(const uint8_t *p, uint32_t (&w)[4]) {
-    if constexpr (M == 16) {
+// MT = compile-time number of parts (8 or 16, the BASELINE configs), or 0
+// for the generic path where M (even, <= 16) is a runtime value.
+template <int MT>
+__device__ __forceinline__ void load_code(const uint8_t *p, uint32_t (&w)[4], int M) {
+    if constexpr (MT == 16) {
         uint4 v = __ldg(reinterpret_cast<const uint4 *>(p));
         w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
-    } else if constexpr (M == 8) {
+    } else if constexpr (MT == 8) {
         uint2 v = __ldg(reinterpret_cast<const uint2 *>(p));
         w[0] = v.x; w[1] = v.y; w[2] = 0; w[3] = 0;
-    } else if constexpr (M % 4 == 0) {
-#pragma unroll
-        for (int i = 0; i < 4; i++) w[i] = i < M / 4 ? __ldg(reinterpret_cast<const uint32_t *>(p) + i) : 0u;
     } else {
 #pragma unroll
         for (int i = 0; i < 4; i++) w[i] = 0;
-#pragma unroll
-        for (int i = 0; i < M / 2; i++) {
-            uint32_t h = __ldg(reinterpret_cast<const uint16_t *>(p) + i);
-            w[i >> 1] |= h << ((i & 1) * 16);
+        if ((M & 3) == 0) {
+            for (int i = 0; i < M / 4; i++) w[i] = __ldg(reinterpret_cast<const uint32_t *>(p) + i);
+        } else {
+            for (int i = 0; i < M / 2; i++) {
+                uint32_t h = __ldg(reinterpret_cast<const uint16_t *>(p) + i);
+                w[i >> 1] |= h << ((i & 1) * 16);
+            }
         }
     }
 }
@@ -280,12 +284,13 @@ __device__ __forceinline__ int code_at(const uint32_t (&w)[4], int p) {
 }
 
 // --------------------------------------------------- per-candidate distances
-template <int M, typename KT, typename OffT>
+template <int MT, typename KT, typename OffT>
 __device__ __forceinline__ float dist_fbpq(const Args<KT, OffT> &A, const float *tab, int oi, int oj,
                                            float cbase, const uint32_t (&w)[4]) {
-    constexpr int M2 = M / 2;
+    const int M = MT ? MT : A.M;
+    const int M2 = M / 2;
     const int K = A.K;
-    float x[M];
+    float x[16];
 #pragma unroll
     for (int p = 0; p < M; p++) {
         const int c = code_at(w, p);
@@ -305,10 +310,11 @@ __device__ __forceinline__ float dist_fbpq(const Args<KT, OffT> &A, const float 
 // Multi-D-ADC explicit reconstruction (ENGINE 0) and HBPQ local books
 // (ENGINE 2): e = q_h - c_h[row] (one rounding, multi_index.py:345-346),
 // d = e - book, acc += d*d sequentially (numba_backend.py:165-176, 198-210).
-template <int ENGINE, int M, typename KT, typename OffT>
+template <int ENGINE, int MT, typename KT, typename OffT>
 __device__ __forceinline__ float dist_recon(const Args<KT, OffT> &A, const float *tab, int oi, int oj,
                                             const uint32_t (&w)[4]) {
-    constexpr int M2 = M / 2;
+    const int M = MT ? MT : A.M;
+    const int M2 = M / 2;
     const int K = A.K, ds = A.ds, dh = A.dh;
     float acc = 0.f;
 #pragma unroll
@@ -437,7 +443,7 @@ __device__ void topk_compact(Smem &S, int k) {
 // key(b + 1, b) exceeds tau, so a count or a band touches only O(active
 // rows + active columns) lines even when the region is a long thin "L"
 // (one very close codeword per half, which the BASELINE mixture produces).
-template <int ENGINE, int M, typename KT, typename OffT>
+template <int ENGINE, int MT, typename KT, typename OffT>
 struct Query {
     const Args<KT, OffT> &A;
     Smem &S;
@@ -449,7 +455,7 @@ struct Query {
     const int32_t *o1, *o2;  // sorted position -> codeword
     const int32_t *p1, *p2;  // codeword -> sorted position
     const float *d1, *d2;
-    int T, P;
+    int T, P, M;
     unsigned long long ncand;  // uniform across the CTA
     unsigned long long popped;
 
@@ -457,6 +463,7 @@ struct Query {
                      const KT *s1, const KT *s2)
         : A(a), S(s), qi(q), s1s(s1), s2s(s2), tab(tab_), lut(lut_) {
         T = A.T;
+        M = MT ? MT : A.M;
         P = A.sr_smem;
         sr1 = A.sr1 + q * T;
         sr2 = A.sr2 + q * T;
@@ -513,7 +520,7 @@ struct Query {
     __device__ void scan_cell_lut(int oi, int oj, uint32_t lst, uint32_t lc, float cb) {
         const int pv = PROF(PH_LUT);
         (void)pv;
-        constexpr int M2 = M / 2;
+        const int M2 = M / 2;
         const int K = A.K;
         for (int idx = threadIdx.x; idx < M * K; idx += NT) {
             const int p = idx / K, c = idx - p * K;
@@ -529,7 +536,7 @@ struct Query {
             for (int u = 0; u < kUnroll; u++) {
                 const uint32_t e = e0 + u * NT + threadIdx.x;
                 if (e < lc) {
-                    load_code<M>(A.codes + (size_t)(lst + e) * M, w[u]);
+                    load_code<MT>(A.codes + (size_t)(lst + e) * M, w[u], M);
                     idv[u] = __ldg(A.ids + lst + e);
                 }
             }
@@ -621,7 +628,7 @@ struct Query {
                             }
                             own[u] = lo;
                             entry[u] = S.cstart[lo] + (e - S.cpre[lo]);
-                            load_code<M>(A.codes + (size_t)entry[u] * M, w[u]);
+                            load_code<MT>(A.codes + (size_t)entry[u] * M, w[u], M);
                             idv[u] = __ldg(A.ids + entry[u]);
                         }
                     }
@@ -631,9 +638,9 @@ struct Query {
                         const int lo = own[u];
                         float dist;
                         if constexpr (ENGINE == BPQ_ENGINE_FBPQ)
-                            dist = dist_fbpq<M>(A, tab, S.coi[lo], S.coj[lo], S.cbase[lo], w[u]);
+                            dist = dist_fbpq<MT>(A, tab, S.coi[lo], S.coj[lo], S.cbase[lo], w[u]);
                         else
-                            dist = dist_recon<ENGINE, M>(A, tab, S.coi[lo], S.coj[lo], w[u]);
+                            dist = dist_recon<ENGINE, MT>(A, tab, S.coi[lo], S.coj[lo], w[u]);
                         offer(dist, idv[u]);
                     }
                     round_end();
@@ -758,6 +765,38 @@ struct Query {
             }
         }
         return block_sum_u64(S, cnt);
+    }
+
+    // C(tau) at NW thresholds at once: warp w evaluates S.mtau[w] over its
+    // active lines.  Returns false when some threshold activates more than
+    // kMultiLines lines (the caller then falls back to count_le).
+    __device__ bool count_multi(const int32_t *rowB, int RA, const int32_t *colB, int CA) {
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        const double tau = S.mtau[warp];
+        const int nr = warp_first_false([&](int a) { return k1(a) + k2(a) <= tau; }, 0, T);
+        const int nc = warp_first_false([&](int b) { return k1(b + 1) + k2(b) <= tau; }, 0, T - 1);
+        unsigned long long cnt = 0;
+        const bool ok = nr + nc <= kMultiLines;
+        if (ok) {
+            for (int line = 0; line < nr + nc; line++) {
+                if (line < nr) {
+                    const double ka = k1(line);
+                    const int B = warp_first_false([&](int x) { return ka + k2(x) <= tau; }, row_lo(rowB, RA, line), T);
+                    cnt += (unsigned)(B - line);
+                } else {
+                    const int b = line - nr;
+                    const double kb = k2(b);
+                    const int Av = warp_first_false([&](int x) { return k1(x) + kb <= tau; }, col_lo(colB, CA, b), T);
+                    cnt += (unsigned)(Av - (b + 1));
+                }
+            }
+        }
+        if (lane == 0) S.mcnt[warp] = ok ? cnt : ~0ull;
+        __syncthreads();
+        bool all = true;
+#pragma unroll
+        for (int w = 0; w < NW; w++) all = all && S.mcnt[w] != ~0ull;
+        return all;
     }
 
     // exact cutoff inside the final band (weighted select, then smem sort)
@@ -946,6 +985,159 @@ struct Query {
         return block_sum_u64(S, wb);
     }
 
+    // ------------------------------------------------------------------
+    // Sparse-table traversal (populated-cell lists present).  Lines become
+    // active in order of their diagonal key (row a: key(a, a); column b:
+    // key(b + 1, b)); activating a line moves its populated cells of its half
+    // of the staircase into a pending pool.  With kappa = the smallest
+    // activation key of a line not yet active, every populated cell with
+    // key < kappa is in the pool, so those cells form the next band: scanned
+    // whole while the running total stays < L, else the exact cutoff is
+    // selected inside them.  No threshold search and no empty cell is ever
+    // touched.  Returns false (nothing emitted) if the pool would overflow;
+    // the caller then falls back to the band traversal.
+    __device__ __forceinline__ double act_row(int a) const { return a < T ? k1(a) + k2(a) : INFINITY; }
+    __device__ __forceinline__ double act_col(int b) const { return b < T - 1 ? k1(b + 1) + k2(b) : INFINITY; }
+
+    __device__ bool run_sparse(int4 *band, int4 *pend, int4 *pend2, int4 *other) {
+        const unsigned long long L = (unsigned long long)A.L;
+        unsigned long long W = 0;
+        int nr = 0, nc = 0, npend = 0;
+        int NB = 32;
+        for (;;) {
+            // next NB lines in activation order (merge path over the two sequences)
+            if (threadIdx.x < 32) {
+                const int x = warp_first_false(
+                    [&](int xx) { return act_row(nr + xx) <= act_col(nc + NB - 1 - xx); }, 0, NB);
+                if (threadIdx.x == 0) {
+                    int nr2 = min(nr + x, T), nc2 = min(nc + (NB - x), T - 1);
+                    S.cnt_nr = nr2;
+                    S.cnt_nc = nc2;
+                }
+            }
+            __syncthreads();
+            const int nr2 = S.cnt_nr, nc2 = S.cnt_nc;
+            const double kappa = fmin(act_row(nr2), act_col(nc2));
+            if (threadIdx.x == 0) {
+                S.nlist = 0;
+                S.tcnt = 0;
+            }
+            __syncthreads();
+            // gather newly active lines' cells (one line per thread, flattened)
+            unsigned long long wb = 0;
+            const int nnew = (nr2 - nr) + (nc2 - nc);
+            for (int base = 0; base < nnew; base += NT) {
+                const int v = base + threadIdx.x;
+                uint32_t nnz = 0, p0 = 0, line = 0;
+                int idx = 0;
+                bool col = false;
+                if (v < nnew) {
+                    col = v >= nr2 - nr;
+                    idx = col ? nc + (v - (nr2 - nr)) : nr + v;
+                    line = (uint32_t)__ldg((col ? o2 : o1) + idx);
+                    const uint32_t *ptr = col ? A.colptr : A.rowptr;
+                    p0 = __ldg(ptr + line);
+                    nnz = __ldg(ptr + line + 1) - p0;
+                }
+                uint32_t E;
+                const uint32_t ex = block_excl_scan(S, nnz, &E);
+                S.cpre[threadIdx.x] = ex;
+                S.cstart[threadIdx.x] = p0;
+                S.coi[threadIdx.x] = (int)line;
+                S.coj[threadIdx.x] = col ? -(idx + 1) : idx;
+                __syncthreads();
+                for (uint32_t e = threadIdx.x; e < E; e += NT) {
+                    int lo = 0, hi = NT;
+                    while (hi - lo > 1) {
+                        const int mid = (lo + hi) >> 1;
+                        if (S.cpre[mid] <= e) lo = mid; else hi = mid;
+                    }
+                    const uint32_t t = S.cstart[lo] + (e - S.cpre[lo]);
+                    const uint32_t ln = (uint32_t)S.coi[lo];
+                    const int tag = S.coj[lo];
+                    int a, b;
+                    unsigned long long lin;
+                    bool own;
+                    if (tag >= 0) {  // row a = tag owns columns b >= a
+                        const uint32_t j = A.rowcols[t];
+                        a = tag;
+                        b = __ldg(p2 + j);
+                        own = b >= a;
+                        lin = (unsigned long long)ln * T + j;
+                    } else {  // column b owns rows a > b
+                        const uint32_t i = A.colrows[t];
+                        b = -tag - 1;
+                        a = __ldg(p1 + i);
+                        own = a > b;
+                        lin = (unsigned long long)i * T + ln;
+                    }
+                    if (!own) continue;
+                    const OffT g0 = __ldg(A.goff + lin), g1 = __ldg(A.goff + lin + 1);
+                    if (!(g1 > g0)) continue;
+                    uint32_t lst, lcn;
+                    if (A.sharded) {
+                        const OffT l0 = __ldg(A.loff + lin), l1 = __ldg(A.loff + lin + 1);
+                        lst = (uint32_t)l0;
+                        lcn = (uint32_t)(l1 - l0);
+                    } else {
+                        lst = (uint32_t)g0;
+                        lcn = (uint32_t)(g1 - g0);
+                    }
+                    const int4 cell = make_int4((a << 16) | b, (int)(uint32_t)(g1 - g0), (int)lst, (int)lcn);
+                    if (key(a, b) < kappa) {
+                        const uint32_t pos = atomicAdd(&S.nlist, 1u);
+                        if (pos < (uint32_t)kBandCap) band[pos] = cell;
+                        wb += (unsigned long long)(g1 - g0);
+                    } else {
+                        const uint32_t pos = atomicAdd(&S.tcnt, 1u);
+                        if (pos < (uint32_t)kBandCap) pend2[pos] = cell;
+                    }
+                }
+                __syncthreads();
+            }
+            // re-classify the pool against the new kappa
+            for (int c = threadIdx.x; c < npend; c += NT) {
+                const int4 cell = pend[c];
+                const int a = (unsigned)cell.x >> 16, b = cell.x & 0xFFFF;
+                if (key(a, b) < kappa) {
+                    const uint32_t pos = atomicAdd(&S.nlist, 1u);
+                    if (pos < (uint32_t)kBandCap) band[pos] = cell;
+                    wb += (unsigned long long)(uint32_t)cell.y;
+                } else {
+                    const uint32_t pos = atomicAdd(&S.tcnt, 1u);
+                    if (pos < (uint32_t)kBandCap) pend2[pos] = cell;
+                }
+            }
+            wb = block_sum_u64(S, wb);
+            const uint32_t nband = S.nlist, npend2 = S.tcnt;
+            if (nband > (uint32_t)kBandCap || npend2 > (uint32_t)kBandCap) return false;
+            if (W + wb < L) {
+                emit(band, (int)nband, -1, 0);
+                W += wb;
+                if (!(kappa < INFINITY)) {
+                    popped = (unsigned long long)T * T;
+                    return true;
+                }
+            } else {
+                final_select(band, other, (int)nband, L - W);
+                if (A.out_popped) {
+                    __syncthreads();
+                    popped = count_le(__longlong_as_double((long long)S.cut_key), nullptr, 0, nullptr, 0,
+                                      nullptr, nullptr);
+                }
+                return true;
+            }
+            int4 *t = pend;
+            pend = pend2;
+            pend2 = t;
+            npend = (int)npend2;
+            nr = nr2;
+            nc = nc2;
+            NB = min(NB * 2, NT);
+            __syncthreads();
+        }
+    }
+
     __device__ void run() {
         char *scr = A.scratch + (size_t)blockIdx.x * A.stride;
         int32_t *rowB = reinterpret_cast<int32_t *>(scr);
@@ -956,6 +1148,8 @@ struct Query {
         uint4 *seg = reinterpret_cast<uint4 *>(scr + (((size_t)6 * T * 4 + 15) & ~(size_t)15));
         int4 *listA = reinterpret_cast<int4 *>(seg + 2 * T);
         int4 *listB = listA + kBandCap;
+        int4 *listC = listB + kBandCap;
+        int4 *listD = listC + kBandCap;
 
         if (threadIdx.x == 0) {
             S.ntk = 0;
@@ -964,6 +1158,17 @@ struct Query {
         }
         __syncthreads();
         if (A.n_global == 0) return;
+        if (A.rowptr != nullptr) {
+            if (run_sparse(listA, listB, listC, listD)) return;
+            // pool overflow: restart this query with the band traversal
+            ncand = 0;
+            popped = 0;
+            if (threadIdx.x == 0) {
+                S.ntk = 0;
+                S.thr = ~0ull;
+            }
+            __syncthreads();
+        }
 
         const bool lists = A.rowptr != nullptr;
         const unsigned long long Tall = (unsigned long long)T * T;
@@ -990,7 +1195,58 @@ struct Query {
                 cHi = chi;
                 const double want = (double)Cprev + target;
                 PROF(PH_TAU);
-                for (int it = 0; it < 200; it++) {
+                // multi-probe rounds: NW thresholds per round, one per warp
+                for (int round = 0; round < 8 && !accepted; round++) {
+                    const double xlo = fmax(lo - k00, 0.0), xhi = hi - k00;
+                    if (!(xhi > 0.0)) break;
+                    __syncthreads();  // previous round's S.mtau / S.mcnt fully consumed
+                    if (threadIdx.x < NW) {
+                        const int w = threadIdx.x;
+                        double x;
+                        if (xlo > 0.0) {
+                            x = xlo * pow(xhi / xlo, (double)(w + 1) / (NW + 1));
+                        } else {
+                            const double fr[NW] = {1.0 / 4096, 1.0 / 1024, 1.0 / 256, 1.0 / 64,
+                                                   1.0 / 16, 1.0 / 4, 0.5, 0.75};
+                            x = xhi * fr[w];
+                        }
+                        double t = k00 + x;
+                        if (!(t > lo)) t = lo + (hi - lo) * (w + 1) / (NW + 1);
+                        if (!(t < hi)) t = hi;
+                        S.mtau[w] = t;
+                    }
+                    __syncthreads();
+                    if (!count_multi(rowB, RA, colB, CA)) break;
+                    // best accepted probe, else the tightest bracket
+                    double nlo = lo, nhi = hi;
+                    unsigned long long nclo = clo, nchi = chi;
+                    int acc_w = -1;
+                    for (int w = 0; w < NW; w++) {
+                        const double t = S.mtau[w];
+                        const unsigned long long cm = S.mcnt[w];
+                        if (!(t > lo && t < hi)) continue;
+                        const double band = (double)(cm - Cprev);
+                        if (band > target) {
+                            if (t < nhi) { nhi = t; nchi = cm; }
+                        } else if (band < 0.5 * target) {
+                            if (t > nlo) { nlo = t; nclo = cm; }
+                        } else {
+                            acc_w = w;  // largest accepted probe wins
+                        }
+                    }
+                    if (acc_w >= 0) {
+                        tauHi = S.mtau[acc_w];
+                        cHi = S.mcnt[acc_w];
+                        accepted = true;
+                    } else {
+                        if (nlo == lo && nhi == hi) break;  // no progress possible
+                        lo = nlo;
+                        hi = nhi;
+                        clo = nclo;
+                        chi = nchi;
+                    }
+                }
+                for (int it = 0; it < 200 && !accepted; it++) {
                     const double xlo = fmax(lo - k00, 0.0), xhi = hi - k00;
                     if (!(xhi > 0.0)) break;
                     double mid;
@@ -1172,8 +1428,9 @@ struct Query {
     }
 };
 
-template <int ENGINE, int M, typename KT, typename OffT>
+template <int ENGINE, int MT, typename KT, typename OffT>
 __global__ void __launch_bounds__(NT, BPQ_MINB) search_kernel(Args<KT, OffT> A) {
+    const int M = MT ? MT : A.M;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem &S = *reinterpret_cast<Smem *>(smem_raw);
     float *tab = reinterpret_cast<float *>(smem_raw + sizeof(Smem));
@@ -1229,7 +1486,7 @@ __global__ void __launch_bounds__(NT, BPQ_MINB) search_kernel(Args<KT, OffT> A) 
             }
         }
         __syncthreads();
-        Query<ENGINE, M, KT, OffT> Q(A, S, qi, tab, lut, s1s, s2s);
+        Query<ENGINE, MT, KT, OffT> Q(A, S, qi, tab, lut, s1s, s2s);
         Q.run();
         Q.finish();
         __syncthreads();
@@ -1253,10 +1510,10 @@ int num_sms() {
     return g_num_sms;
 }
 
-template <int ENGINE, int M, typename KT, typename OffT>
+template <int ENGINE, int MT, typename KT, typename OffT>
 int configure(size_t smem, int *n_cta_out) {
     static bool attr = false;
-    auto kfn = search_kernel<ENGINE, M, KT, OffT>;
+    auto kfn = search_kernel<ENGINE, MT, KT, OffT>;
     if (!attr) {
         int dev = 0, optin = 0;
         BPQ_CUDA_TRY(cudaGetDevice(&dev));
@@ -1271,17 +1528,18 @@ int configure(size_t smem, int *n_cta_out) {
     return BPQ_OK;
 }
 
-template <int ENGINE, int M>
+template <int ENGINE, int MT>
 int launch_one(const Index &ix, const float *queries, int64_t q0, int64_t nq, int64_t budget,
                int32_t k, const SearchWorkspace &ws, float *out_dist, uint32_t *out_ids,
                int32_t *out_count, int64_t *out_ncand, int64_t *out_popped, cudaStream_t stream) {
     Args<float, uint32_t> A{};
-    A.tab_floats = ENGINE == BPQ_ENGINE_FBPQ ? 2 * M * ix.K : ix.D;  // fold + per-cell LUT
+    A.M = ix.M;
+    A.tab_floats = ENGINE == BPQ_ENGINE_FBPQ ? 2 * ix.M * ix.K : ix.D;  // fold + per-cell LUT
     A.tab_floats = (A.tab_floats + 3) & ~3;
     A.sr_smem = 0;  // sorted keys are read through L1: only active lines are probed
     const size_t smem = dyn_smem_bytes(A.tab_floats, A.sr_smem, sizeof(float));
     int n_cta = 0;
-    int rc = configure<ENGINE, M, float, uint32_t>(smem, &n_cta);
+    int rc = configure<ENGINE, MT, float, uint32_t>(smem, &n_cta);
     if (rc) return rc;
     if (n_cta > ws.n_cta) n_cta = ws.n_cta;
     A.T = ix.T;
@@ -1333,7 +1591,7 @@ int launch_one(const Index &ix, const float *queries, int64_t q0, int64_t nq, in
     A.scratch = ws.cta_scratch;
     A.stride = ws.cta_stride;
     BPQ_CUDA_TRY(cudaMemsetAsync(ws.counter, 0, sizeof(unsigned int), stream));
-    search_kernel<ENGINE, M, float, uint32_t><<<n_cta, NT, smem, stream>>>(A);
+    search_kernel<ENGINE, MT, float, uint32_t><<<n_cta, NT, smem, stream>>>(A);
     BPQ_CUDA_TRY(cudaGetLastError());
     return BPQ_OK;
 }
@@ -1343,14 +1601,10 @@ int dispatch_m(const Index &ix, const float *queries, int64_t q0, int64_t nq, in
                int32_t k, const SearchWorkspace &ws, float *od, uint32_t *oi, int32_t *oc,
                int64_t *on, int64_t *op, cudaStream_t s) {
     switch (ix.M) {
-        case 2: return launch_one<ENGINE, 2>(ix, queries, q0, nq, budget, k, ws, od, oi, oc, on, op, s);
-        case 4: return launch_one<ENGINE, 4>(ix, queries, q0, nq, budget, k, ws, od, oi, oc, on, op, s);
-        case 6: return launch_one<ENGINE, 6>(ix, queries, q0, nq, budget, k, ws, od, oi, oc, on, op, s);
         case 8: return launch_one<ENGINE, 8>(ix, queries, q0, nq, budget, k, ws, od, oi, oc, on, op, s);
-        case 10: return launch_one<ENGINE, 10>(ix, queries, q0, nq, budget, k, ws, od, oi, oc, on, op, s);
-        case 12: return launch_one<ENGINE, 12>(ix, queries, q0, nq, budget, k, ws, od, oi, oc, on, op, s);
-        case 14: return launch_one<ENGINE, 14>(ix, queries, q0, nq, budget, k, ws, od, oi, oc, on, op, s);
         case 16: return launch_one<ENGINE, 16>(ix, queries, q0, nq, budget, k, ws, od, oi, oc, on, op, s);
+        case 2: case 4: case 6: case 10: case 12: case 14:
+            return launch_one<ENGINE, 0>(ix, queries, q0, nq, budget, k, ws, od, oi, oc, on, op, s);
     }
     return fail(BPQ_ERR_UNSUPPORTED, "num_parts must be even and in [2, 16]");
 }
