@@ -31,6 +31,7 @@ constexpr int kSearchThreads = 256;     // threads per CTA (one CTA per query at
 constexpr int kTopkBuf = 2048;          // per-CTA top-k candidate buffer (u64 keys)
 constexpr int kMaxK = kTopkBuf - 4 * kSearchThreads;  // largest k the engine accepts
 constexpr int kSortCap = 512;           // final-band cells sorted in shared memory
+constexpr int kTopP = 1024;             // sorted prefix per half for sparse-table queries
 constexpr int kMultiLines = 8;          // lines a warp evaluates per threshold in a multi-probe round
 constexpr int kLutMin = 96;             // cells with >= this many entries are scanned via a smem LUT
 constexpr int kBandCap = 32768;         // max cells enumerated per band
@@ -55,14 +56,23 @@ struct Index {
 int launch_coarse_dots(const float *queries, int64_t nq, int32_t D, const float *c1,
                        const float *c2, int32_t T, float *dots1, float *dots2,
                        cudaStream_t stream);
+int launch_fold(const float *queries, int64_t nq, int32_t D, int32_t M, int32_t K, const float *books,
+                const float *fine_norms, float *fold, cudaStream_t stream);
 int launch_row_sort(const float *queries, int64_t nq, int32_t D, const float *dots1,
                     const float *dots2, const float *cn1, const float *cn2, int32_t T,
                     float *sr1, float *sr2, int32_t *ord1, int32_t *ord2, int32_t *pos1,
-                    int32_t *pos2, cudaStream_t stream);
+                    int32_t *pos2, float *ru1, float *ru2, const unsigned int *qlist,
+                    const unsigned int *qcount, cudaStream_t stream);
+int launch_row_topk(const float *queries, int64_t nq, int32_t D, const float *dots1,
+                    const float *dots2, const float *cn1, const float *cn2, int32_t T, float *sr1,
+                    float *sr2, int32_t *ord1, int32_t *ord2, float *ru1, float *ru2, cudaStream_t stream);
 
 struct SearchWorkspace {
-    float *dots1, *dots2, *sr1, *sr2;
+    float *dots1, *dots2, *sr1, *sr2, *fold, *ru1, *ru2;
     int32_t *ord1, *ord2, *pos1, *pos2;
+    unsigned int *retry_list, *retry_count;
+    int topP;                      // sorted prefix length in sr/ord for this launch
+    const unsigned int *qlist, *qlist_count;  // indirect query list (retry pass)
     unsigned int *counter;
     char *cta_scratch;
     size_t cta_stride;

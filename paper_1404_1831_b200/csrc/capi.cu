@@ -22,13 +22,13 @@ size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct SearchLayout {
     int64_t chunk;
-    size_t dots1, dots2, sr1, sr2, ord1, ord2, pos1, pos2, counter, cta, cta_stride, total;
+    size_t dots1, dots2, sr1, sr2, ord1, ord2, pos1, pos2, fold, ru1, ru2, retry, counter, cta, cta_stride, total;
     int n_cta;
 };
 
-int64_t query_chunk(int64_t nq, int32_t T) {
-    // keep the per-chunk first-layer buffers (8 arrays of [chunk, T] x 4 B) near 2 GiB
-    int64_t per_q = (int64_t)T * 32;
+int64_t query_chunk(int64_t nq, int32_t T, int32_t M, int32_t K) {
+    // keep the per-chunk first-layer buffers (10 arrays of [chunk, T] x 4 B + fold) near 2 GiB
+    int64_t per_q = (int64_t)T * 40 + (int64_t)M * K * 4 + 4;
     int64_t c = ((int64_t)2 << 30) / per_q;
     c = std::max<int64_t>(c, 256);
     return std::max<int64_t>(1, std::min<int64_t>(nq, c));
@@ -36,7 +36,7 @@ int64_t query_chunk(int64_t nq, int32_t T) {
 
 bool layout_for(const Index &ix, int64_t nq, SearchLayout *L) {
     SearchLayout s{};
-    s.chunk = query_chunk(nq, ix.T);
+    s.chunk = query_chunk(nq, ix.T, ix.M, ix.K);
     int n_cta = search_grid_ctas(BPQ_ENGINE_FBPQ, ix.M);
     if (n_cta <= 0) return false;
     s.n_cta = n_cta;
@@ -50,6 +50,10 @@ bool layout_for(const Index &ix, int64_t nq, SearchLayout *L) {
     s.ord2 = o; o += al(row);
     s.pos1 = o; o += al(row);
     s.pos2 = o; o += al(row);
+    s.fold = o; o += al((size_t)s.chunk * ix.M * ix.K * 4);
+    s.ru1 = o; o += al(row);
+    s.ru2 = o; o += al(row);
+    s.retry = o; o += al((size_t)s.chunk * 4 + 4);
     s.counter = o; o += al(4);
     s.cta_stride = al(search_cta_scratch_bytes(ix.T));
     s.cta = o; o += s.cta_stride * n_cta;
@@ -244,6 +248,13 @@ extern "C" int bpq_search_ex(const bpq_index *index, int engine, const float *qu
     ws.ord2 = reinterpret_cast<int32_t *>(w + L.ord2);
     ws.pos1 = reinterpret_cast<int32_t *>(w + L.pos1);
     ws.pos2 = reinterpret_cast<int32_t *>(w + L.pos2);
+    ws.fold = reinterpret_cast<float *>(w + L.fold);
+    ws.ru1 = reinterpret_cast<float *>(w + L.ru1);
+    ws.ru2 = reinterpret_cast<float *>(w + L.ru2);
+    ws.retry_count = reinterpret_cast<unsigned int *>(w + L.retry);
+    ws.retry_list = ws.retry_count + 1;
+    ws.qlist = nullptr;
+    ws.qlist_count = nullptr;
     ws.counter = reinterpret_cast<unsigned int *>(w + L.counter);
     ws.cta_scratch = w + L.cta;
     ws.cta_stride = L.cta_stride;
@@ -257,13 +268,45 @@ extern "C" int bpq_search_ex(const bpq_index *index, int engine, const float *qu
         int rc = launch_coarse_dots(qc, n, ix.D, ix.c1, ix.c2, ix.T, ws.dots1, ws.dots2, s);
         if (rc) return rc;
         if (ev) BPQ_CUDA_TRY(cudaEventRecord((cudaEvent_t)stage_events[1], s));
-        rc = launch_row_sort(qc, n, ix.D, ws.dots1, ws.dots2, ix.cn1, ix.cn2, ix.T, ws.sr1, ws.sr2,
-                             ws.ord1, ws.ord2, ws.pos1, ws.pos2, s);
+        // sparse tables only need the activated lines' sorted prefix: partial
+        // sort first, full sort only for queries that outgrow it (retry pass)
+        const bool sparse = ix.rowptr != nullptr;
+        const bool partial = sparse && ix.T > kTopP && out_popped == nullptr;
+        if (partial) {
+            rc = launch_row_topk(qc, n, ix.D, ws.dots1, ws.dots2, ix.cn1, ix.cn2, ix.T, ws.sr1, ws.sr2,
+                                 ws.ord1, ws.ord2, ws.ru1, ws.ru2, s);
+        } else {
+            rc = launch_row_sort(qc, n, ix.D, ws.dots1, ws.dots2, ix.cn1, ix.cn2, ix.T, ws.sr1, ws.sr2,
+                                 ws.ord1, ws.ord2, ws.pos1, ws.pos2, sparse ? ws.ru1 : nullptr,
+                                 sparse ? ws.ru2 : nullptr, nullptr, nullptr, s);
+        }
         if (rc) return rc;
+        ws.topP = partial ? kTopP : ix.T;
+        BPQ_CUDA_TRY(cudaMemsetAsync(ws.retry_count, 0, 4, s));
+        if (engine == BPQ_ENGINE_FBPQ) {
+            rc = launch_fold(qc, n, ix.D, ix.M, ix.K, ix.books, ix.fine_norms, ws.fold, s);
+            if (rc) return rc;
+        }
         if (ev) BPQ_CUDA_TRY(cudaEventRecord((cudaEvent_t)stage_events[2], s));
         rc = launch_search(ix, engine, qc, q0, n, budget, k, ws, out_dist, out_ids, out_count,
                            out_ncand, out_popped, s);
         if (rc) return rc;
+        if (partial) {
+            // retry pass: full sort + search for the queued queries (device-side list)
+            rc = launch_row_sort(qc, n, ix.D, ws.dots1, ws.dots2, ix.cn1, ix.cn2, ix.T, ws.sr1, ws.sr2,
+                                 ws.ord1, ws.ord2, ws.pos1, ws.pos2, ws.ru1, ws.ru2, ws.retry_list,
+                                 ws.retry_count, s);
+            if (rc) return rc;
+            SearchWorkspace w2 = ws;
+            w2.topP = ix.T;
+            w2.qlist = ws.retry_list;
+            w2.qlist_count = ws.retry_count;
+            w2.retry_list = nullptr;
+            w2.retry_count = nullptr;
+            rc = launch_search(ix, engine, qc, q0, n, budget, k, w2, out_dist, out_ids, out_count,
+                               out_ncand, out_popped, s);
+            if (rc) return rc;
+        }
         if (ev) BPQ_CUDA_TRY(cudaEventRecord((cudaEvent_t)stage_events[3], s));
     }
     return BPQ_OK;

@@ -129,7 +129,11 @@ struct Args {
     unsigned long long n_global;
     const float *queries;
     int64_t q0, nq;
-    const float *dots1, *dots2;
+    const float *dots1, *dots2, *fold;
+    const float *ru1, *ru2;          // unsorted half-distances [nq, T] (sparse mode)
+    int topP;                        // sorted prefix length available in sr/ord
+    unsigned int *retry_list, *retry_count;   // queries needing the full sort
+    const unsigned int *qlist, *qlist_count;  // indirect query list (retry pass)
     const KT *sr1, *sr2;
     const int32_t *ord1, *ord2;
     const int32_t *pos1, *pos2;
@@ -455,6 +459,8 @@ struct Query {
     const int32_t *o1, *o2;  // sorted position -> codeword
     const int32_t *p1, *p2;  // codeword -> sorted position
     const float *d1, *d2;
+    const float *u1, *u2;    // unsorted half-distances (codeword-keyed entries)
+    bool cw;                 // list entries hold codewords (i, j) instead of positions (a, b)
     int T, P, M;
     unsigned long long ncand;  // uniform across the CTA
     unsigned long long popped;
@@ -473,6 +479,9 @@ struct Query {
         p2 = A.pos2 ? A.pos2 + q * T : nullptr;
         d1 = A.dots1 ? A.dots1 + q * T : nullptr;
         d2 = A.dots2 ? A.dots2 + q * T : nullptr;
+        u1 = A.ru1 ? A.ru1 + q * T : nullptr;
+        u2 = A.ru2 ? A.ru2 + q * T : nullptr;
+        cw = false;
         ncand = 0;
         popped = 0;
     }
@@ -485,14 +494,35 @@ struct Query {
         return (unsigned long long)__ldg(o1 + a) * (unsigned long long)T + (unsigned)__ldg(o2 + b);
     }
 
+    // List entries: x = (hi << 16) | lo, positions (a, b) in the band
+    // traversal or codewords (i, j) in the sparse one (cw).  Both give the
+    // same key value: f64(r1[i]) + f64(r2[j]) == f64(sr1[a]) + f64(sr2[b]).
+    __device__ __forceinline__ double ekey(int4 e) const {
+        const int x = (unsigned)e.x >> 16, y = e.x & 0xFFFF;
+        return cw ? (double)__ldg(u1 + x) + (double)__ldg(u2 + y) : key(x, y);
+    }
+    __device__ __forceinline__ unsigned long long elin(int4 e) const {
+        const int x = (unsigned)e.x >> 16, y = e.x & 0xFFFF;
+        return cw ? (unsigned long long)x * T + (unsigned)y : lin_of(x, y);
+    }
+    __device__ __forceinline__ void eij(int4 e, int &oi, int &oj) const {
+        const int x = (unsigned)e.x >> 16, y = e.x & 0xFFFF;
+        if (cw) {
+            oi = x;
+            oj = y;
+        } else {
+            oi = __ldg(o1 + x);
+            oj = __ldg(o2 + y);
+        }
+    }
+
     // 12-byte composite sort key digit d (0 = most significant)
     __device__ __forceinline__ int digit(int d, int4 e) const {
-        int a = (unsigned)e.x >> 16, b = e.x & 0xFFFF;
         if (d < 8) {
-            unsigned long long kb = (unsigned long long)__double_as_longlong(key(a, b));
+            unsigned long long kb = (unsigned long long)__double_as_longlong(ekey(e));
             return (int)((kb >> (56 - 8 * d)) & 0xFF);
         }
-        unsigned long long lin = lin_of(a, b);
+        unsigned long long lin = elin(e);
         return (int)((lin >> (24 - 8 * (d - 8))) & 0xFF);
     }
 
@@ -575,15 +605,12 @@ struct Query {
                 int4 e = list[c];
                 bool pass = filt_d < 0 || digit(filt_d, e) < filt_v;
                 if (pass) {
-                    const int a = (unsigned)e.x >> 16;
-                    const int b = e.x & 0xFFFF;
-                    oi = __ldg(o1 + a);
-                    oj = __ldg(o2 + b);
+                    eij(e, oi, oj);
                     lst = (uint32_t)e.z;
                     lc = (uint32_t)e.w;
                     if constexpr (ENGINE == ENGINE_TRAVERSE) {
                         unsigned long long pos = atomicAdd(A.tv_n, 1ull);
-                        A.tv_key[pos] = (unsigned long long)__double_as_longlong(key(a, b));
+                        A.tv_key[pos] = (unsigned long long)__double_as_longlong(ekey(e));
                         A.tv_lin[pos] = (uint32_t)oi * (uint32_t)T + (uint32_t)oj;
                         A.tv_start[pos] = (int64_t)lst;
                         A.tv_end[pos] = (int64_t)lst + lc;
@@ -809,9 +836,8 @@ struct Query {
                 for (int c = threadIdx.x; c < P2; c += NT) {
                     if (c < n) {
                         int4 e = cur[c];
-                        int a = (unsigned)e.x >> 16, b = e.x & 0xFFFF;
-                        S.skey[c] = (unsigned long long)__double_as_longlong(key(a, b));
-                        S.slin[c] = (uint32_t)lin_of(a, b);
+                        S.skey[c] = (unsigned long long)__double_as_longlong(ekey(e));
+                        S.slin[c] = (uint32_t)elin(e);
                     } else {
                         S.skey[c] = ~0ull;
                         S.slin[c] = ~0u;
@@ -999,20 +1025,28 @@ struct Query {
     __device__ __forceinline__ double act_row(int a) const { return a < T ? k1(a) + k2(a) : INFINITY; }
     __device__ __forceinline__ double act_col(int b) const { return b < T - 1 ? k1(b + 1) + k2(b) : INFINITY; }
 
-    __device__ bool run_sparse(int4 *band, int4 *pend, int4 *pend2, int4 *other) {
+    // Returns 1 when done, 0 when the pool overflowed (nothing emitted is
+    // kept: the caller restarts with the band traversal), 2 when activation
+    // needs more sorted positions than the partial sort provided (the query
+    // is queued for the full-sort retry pass).
+    __device__ int run_sparse(int4 *band, int4 *pend, int4 *pend2, int4 *other) {
         const unsigned long long L = (unsigned long long)A.L;
+        const bool partial = A.topP < T;
+        cw = true;
         unsigned long long W = 0;
         int nr = 0, nc = 0, npend = 0;
         int NB = 32;
         for (;;) {
+            // the batch probes rows < nr + NB and columns < nc + NB (column b
+            // reads position b + 1): stay inside the sorted prefix
+            if (partial && (nr + NB >= A.topP || nc + NB + 1 >= A.topP)) return 2;
             // next NB lines in activation order (merge path over the two sequences)
             if (threadIdx.x < 32) {
                 const int x = warp_first_false(
                     [&](int xx) { return act_row(nr + xx) <= act_col(nc + NB - 1 - xx); }, 0, NB);
                 if (threadIdx.x == 0) {
-                    int nr2 = min(nr + x, T), nc2 = min(nc + (NB - x), T - 1);
-                    S.cnt_nr = nr2;
-                    S.cnt_nc = nc2;
+                    S.cnt_nr = min(nr + x, T);
+                    S.cnt_nc = min(nc + (NB - x), T - 1);
                 }
             }
             __syncthreads();
@@ -1055,23 +1089,25 @@ struct Query {
                     const uint32_t t = S.cstart[lo] + (e - S.cpre[lo]);
                     const uint32_t ln = (uint32_t)S.coi[lo];
                     const int tag = S.coj[lo];
-                    int a, b;
-                    unsigned long long lin;
+                    uint32_t ci, cj;
                     bool own;
-                    if (tag >= 0) {  // row a = tag owns columns b >= a
-                        const uint32_t j = A.rowcols[t];
-                        a = tag;
-                        b = __ldg(p2 + j);
-                        own = b >= a;
-                        lin = (unsigned long long)ln * T + j;
-                    } else {  // column b owns rows a > b
-                        const uint32_t i = A.colrows[t];
-                        b = -tag - 1;
-                        a = __ldg(p1 + i);
-                        own = a > b;
-                        lin = (unsigned long long)i * T + ln;
+                    if (tag >= 0) {  // row position a = tag owns columns of rank >= a
+                        const int a = tag;
+                        cj = A.rowcols[t];
+                        ci = ln;
+                        const float rj = __ldg(u2 + cj), ra = (float)k2(a);
+                        const uint32_t oa = (uint32_t)__ldg(o2 + a);
+                        own = rj > ra || (rj == ra && cj >= oa);
+                    } else {  // column position b owns rows of rank > b
+                        const int b = -tag - 1;
+                        ci = A.colrows[t];
+                        cj = ln;
+                        const float ri = __ldg(u1 + ci), rb = (float)k1(b);
+                        const uint32_t ob = (uint32_t)__ldg(o1 + b);
+                        own = ri > rb || (ri == rb && ci > ob);
                     }
                     if (!own) continue;
+                    const unsigned long long lin = (unsigned long long)ci * T + cj;
                     const OffT g0 = __ldg(A.goff + lin), g1 = __ldg(A.goff + lin + 1);
                     if (!(g1 > g0)) continue;
                     uint32_t lst, lcn;
@@ -1083,8 +1119,8 @@ struct Query {
                         lst = (uint32_t)g0;
                         lcn = (uint32_t)(g1 - g0);
                     }
-                    const int4 cell = make_int4((a << 16) | b, (int)(uint32_t)(g1 - g0), (int)lst, (int)lcn);
-                    if (key(a, b) < kappa) {
+                    const int4 cell = make_int4((int)((ci << 16) | cj), (int)(uint32_t)(g1 - g0), (int)lst, (int)lcn);
+                    if ((double)__ldg(u1 + ci) + (double)__ldg(u2 + cj) < kappa) {
                         const uint32_t pos = atomicAdd(&S.nlist, 1u);
                         if (pos < (uint32_t)kBandCap) band[pos] = cell;
                         wb += (unsigned long long)(g1 - g0);
@@ -1098,8 +1134,7 @@ struct Query {
             // re-classify the pool against the new kappa
             for (int c = threadIdx.x; c < npend; c += NT) {
                 const int4 cell = pend[c];
-                const int a = (unsigned)cell.x >> 16, b = cell.x & 0xFFFF;
-                if (key(a, b) < kappa) {
+                if (ekey(cell) < kappa) {
                     const uint32_t pos = atomicAdd(&S.nlist, 1u);
                     if (pos < (uint32_t)kBandCap) band[pos] = cell;
                     wb += (unsigned long long)(uint32_t)cell.y;
@@ -1110,13 +1145,13 @@ struct Query {
             }
             wb = block_sum_u64(S, wb);
             const uint32_t nband = S.nlist, npend2 = S.tcnt;
-            if (nband > (uint32_t)kBandCap || npend2 > (uint32_t)kBandCap) return false;
+            if (nband > (uint32_t)kBandCap || npend2 > (uint32_t)kBandCap) return 0;
             if (W + wb < L) {
                 emit(band, (int)nband, -1, 0);
                 W += wb;
                 if (!(kappa < INFINITY)) {
                     popped = (unsigned long long)T * T;
-                    return true;
+                    return 1;
                 }
             } else {
                 final_select(band, other, (int)nband, L - W);
@@ -1125,7 +1160,7 @@ struct Query {
                     popped = count_le(__longlong_as_double((long long)S.cut_key), nullptr, 0, nullptr, 0,
                                       nullptr, nullptr);
                 }
-                return true;
+                return 1;
             }
             int4 *t = pend;
             pend = pend2;
@@ -1158,8 +1193,19 @@ struct Query {
         }
         __syncthreads();
         if (A.n_global == 0) return;
-        if (A.rowptr != nullptr) {
-            if (run_sparse(listA, listB, listC, listD)) return;
+        if (A.rowptr != nullptr && A.ru1 != nullptr) {
+            const int rs = run_sparse(listA, listB, listC, listD);
+            if (rs == 1) return;
+            cw = false;
+            if (rs == 2 || A.topP < T) {
+                // needs the full sort: queue for the retry pass (outputs written there)
+                if (threadIdx.x == 0) {
+                    S.err = 2;
+                    A.retry_list[atomicAdd(A.retry_count, 1u)] = (unsigned int)qi;
+                }
+                __syncthreads();
+                return;
+            }
             // pool overflow: restart this query with the band traversal
             ncand = 0;
             popped = 0;
@@ -1389,6 +1435,7 @@ struct Query {
         __syncthreads();
         const int k = A.k;
         const int64_t qo = A.q0 + qi;
+        if (S.err == 2) return;  // re-run by the full-sort retry pass
         if (S.err) {
             for (int x = threadIdx.x; x < k; x += NT) {
                 A.out_d[qo * k + x] = INFINITY;
@@ -1444,7 +1491,14 @@ __global__ void __launch_bounds__(NT, BPQ_MINB) search_kernel(Args<KT, OffT> A) 
     }
 #endif
     for (;;) {
-        if (threadIdx.x == 0) S.qidx = (int64_t)atomicAdd(A.counter, 1u);
+        if (threadIdx.x == 0) {
+            const unsigned int c = atomicAdd(A.counter, 1u);
+            if (A.qlist == nullptr) {
+                S.qidx = (int64_t)c;
+            } else {
+                S.qidx = c < *A.qlist_count ? (int64_t)A.qlist[c] : A.nq;
+            }
+        }
         __syncthreads();
         const int64_t qi = S.qidx;
         if (qi >= A.nq) {
@@ -1463,15 +1517,14 @@ __global__ void __launch_bounds__(NT, BPQ_MINB) search_kernel(Args<KT, OffT> A) 
         if constexpr (ENGINE != ENGINE_TRAVERSE) {
             const float *q = A.queries + qi * A.D;
             if constexpr (ENGINE == BPQ_ENGINE_FBPQ) {
-                // fold = fine_norms - 2 * (book . q_p)   (fbpq.py:140-143)
-                const int K = A.K, ds = A.ds;
-                for (int idx = threadIdx.x; idx < M * K; idx += NT) {
-                    const int p = idx / K;
-                    const float *bk = A.books + (size_t)idx * ds;
-                    const float *qp = q + p * ds;
-                    float dot = 0.f;
-                    for (int u = 0; u < ds; u++) dot = fmaf(__ldg(bk + u), __ldg(qp + u), dot);
-                    tab[idx] = __fsub_rn(__ldg(A.fine_norms + idx), __fmul_rn(2.f, dot));
+                // fold = fine_norms - 2 * (book . q_p) (fbpq.py:140-143), from fold_kernel
+                const float *fq = A.fold + (size_t)qi * M * A.K;
+                if (((M * A.K) & 3) == 0) {
+                    const float4 *src = reinterpret_cast<const float4 *>(fq);
+                    float4 *dst = reinterpret_cast<float4 *>(tab);
+                    for (int x = threadIdx.x; x < (M * A.K) / 4; x += NT) dst[x] = __ldg(src + x);
+                } else {
+                    for (int x = threadIdx.x; x < M * A.K; x += NT) tab[x] = __ldg(fq + x);
                 }
                 // q_norm = qr @ qr (fbpq.py:144)
                 float part = 0.f;
@@ -1569,6 +1622,14 @@ int launch_one(const Index &ix, const float *queries, int64_t q0, int64_t nq, in
     A.nq = nq;
     A.dots1 = ws.dots1;
     A.dots2 = ws.dots2;
+    A.fold = ws.fold;
+    A.ru1 = ix.rowptr ? ws.ru1 : nullptr;
+    A.ru2 = ix.rowptr ? ws.ru2 : nullptr;
+    A.topP = ws.topP;
+    A.retry_list = ws.retry_list;
+    A.retry_count = ws.retry_count;
+    A.qlist = ws.qlist;
+    A.qlist_count = ws.qlist_count;
     A.sr1 = ws.sr1;
     A.sr2 = ws.sr2;
     A.ord1 = ws.ord1;

@@ -201,6 +201,38 @@ def test_sparse_table_vs_oracle(torch_cuda, oracle):
         check_topk(d, i, c, wd, wi, wc, _qn(q), min_exact_frac=0.9)
 
 
+def test_partial_sort_and_retry_pass(torch_cuda, oracle):
+    """Sparse table with T > 1024: queries start on the partial (top-1024)
+    sort; those whose traversal outgrows it are re-run through the full-sort
+    retry pass.  Results must equal the always-full-sort path and the oracle."""
+    import torch
+
+    from paper_1404_1831_b200 import DeviceIndex
+
+    rng = np.random.default_rng(11)
+    t, dim, m, kk, n = 1500, 32, 4, 16, 30_000
+    cent = rng.normal(scale=6.0, size=(400, dim)).astype(np.float32)
+    base = (cent[rng.integers(0, 400, n)] + rng.normal(size=(n, dim))).astype(np.float32)
+    c1 = base[rng.choice(n, t, replace=False), : dim // 2].copy()
+    c2 = base[rng.choice(n, t, replace=False), dim // 2 :].copy()
+    books = rng.normal(scale=0.4, size=(m, kk, dim // m)).astype(np.float32)
+    off, ids, codes = oracle.build_index(base, c1, c2, books)
+    idx = oracle.Index(c1, c2, off, ids, codes, books=books)
+    dix = DeviceIndex(c1=c1, c2=c2, offsets=off, ids=ids, codes=codes, books=books, tables=idx.tables)
+    assert dix.row_ptr is not None
+    q = (cent[rng.integers(0, 400, 48)] + rng.normal(size=(48, dim))).astype(np.float32)
+    for L, k in ((10, 5), (3000, 50), (n, 20)):
+        part = dix.search(q, L, k, "fbpq", ncand=True)
+        popped = torch.empty(q.shape[0], dtype=torch.int64, device="cuda")
+        full = dix.search(q, L, k, "fbpq", ncand=True, popped=popped)   # popped forces the full sort
+        for x, y in zip(part.numpy(), full.numpy()):
+            np.testing.assert_array_equal(x, y)
+        np.testing.assert_array_equal(part.ncand.cpu().numpy(), full.ncand.cpu().numpy())
+        wd, wi, wc, _ = oracle.search_batch_numpy(idx, "fbpq", q[:16], L, k)
+        d, i, c = part.numpy()
+        check_topk(d[:16], i[:16], c[:16], wd, wi, wc, _qn(q[:16]), min_exact_frac=0.85)
+
+
 def test_empty_index_returns_nothing(torch_cuda):
     from paper_1404_1831_b200 import DeviceIndex
 
