@@ -65,13 +65,15 @@ int launch_row_sort(const float *queries, int64_t nq, int32_t D, const float *do
                     const unsigned int *qcount, cudaStream_t stream);
 int launch_row_topk(const float *queries, int64_t nq, int32_t D, const float *dots1,
                     const float *dots2, const float *cn1, const float *cn2, int32_t T, float *sr1,
-                    float *sr2, int32_t *ord1, int32_t *ord2, float *ru1, float *ru2, cudaStream_t stream);
+                    float *sr2, int32_t *ord1, int32_t *ord2, float *ru1, float *ru2, int32_t *plen,
+                    cudaStream_t stream);
 
 struct SearchWorkspace {
     float *dots1, *dots2, *sr1, *sr2, *fold, *ru1, *ru2;
     int32_t *ord1, *ord2, *pos1, *pos2;
     unsigned int *retry_list, *retry_count;
-    int topP;                      // sorted prefix length in sr/ord for this launch
+    int topP;                      // sorted prefix length in sr/ord for this launch (full: T)
+    int32_t *plen;                 // per (query, half) prefix length of the partial sort
     const unsigned int *qlist, *qlist_count;  // indirect query list (retry pass)
     unsigned int *counter;
     char *cta_scratch;

@@ -22,7 +22,7 @@ size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct SearchLayout {
     int64_t chunk;
-    size_t dots1, dots2, sr1, sr2, ord1, ord2, pos1, pos2, fold, ru1, ru2, retry, counter, cta, cta_stride, total;
+    size_t dots1, dots2, sr1, sr2, ord1, ord2, pos1, pos2, fold, ru1, ru2, retry, plen, counter, cta, cta_stride, total;
     int n_cta;
 };
 
@@ -54,6 +54,7 @@ bool layout_for(const Index &ix, int64_t nq, SearchLayout *L) {
     s.ru1 = o; o += al(row);
     s.ru2 = o; o += al(row);
     s.retry = o; o += al((size_t)s.chunk * 4 + 4);
+    s.plen = o; o += al((size_t)s.chunk * 8);
     s.counter = o; o += al(4);
     s.cta_stride = al(search_cta_scratch_bytes(ix.T));
     s.cta = o; o += s.cta_stride * n_cta;
@@ -253,6 +254,7 @@ extern "C" int bpq_search_ex(const bpq_index *index, int engine, const float *qu
     ws.ru2 = reinterpret_cast<float *>(w + L.ru2);
     ws.retry_count = reinterpret_cast<unsigned int *>(w + L.retry);
     ws.retry_list = ws.retry_count + 1;
+    ws.plen = reinterpret_cast<int32_t *>(w + L.plen);
     ws.qlist = nullptr;
     ws.qlist_count = nullptr;
     ws.counter = reinterpret_cast<unsigned int *>(w + L.counter);
@@ -274,7 +276,7 @@ extern "C" int bpq_search_ex(const bpq_index *index, int engine, const float *qu
         const bool partial = sparse && ix.T > kTopP && out_popped == nullptr;
         if (partial) {
             rc = launch_row_topk(qc, n, ix.D, ws.dots1, ws.dots2, ix.cn1, ix.cn2, ix.T, ws.sr1, ws.sr2,
-                                 ws.ord1, ws.ord2, ws.ru1, ws.ru2, s);
+                                 ws.ord1, ws.ord2, ws.ru1, ws.ru2, ws.plen, s);
         } else {
             rc = launch_row_sort(qc, n, ix.D, ws.dots1, ws.dots2, ix.cn1, ix.cn2, ix.T, ws.sr1, ws.sr2,
                                  ws.ord1, ws.ord2, ws.pos1, ws.pos2, sparse ? ws.ru1 : nullptr,

@@ -19,16 +19,17 @@ namespace bpq {
 
 namespace {
 
-constexpr int BQ = 64, BT = 64, BK = 16;
+constexpr int BQ = 128, BT = 128, BK = 8;
 
 // dots_h[q, t] = sum_x Q[q, h*dh + x] * C_h[t, x]   (h = blockIdx.z)
+// 128x128 output tile per CTA, 8x8 per thread, k staged 8 at a time.
 __global__ void __launch_bounds__(256) coarse_dots_kernel(const float *__restrict__ Q, int64_t nq,
                                                           int D, const float *__restrict__ C1,
                                                           const float *__restrict__ C2, int T,
                                                           float *__restrict__ dots1,
                                                           float *__restrict__ dots2) {
-    __shared__ __align__(16) float Qs[BK][BQ + 4];
-    __shared__ __align__(16) float Cs[BK][BT + 4];
+    __shared__ __align__(16) float Qs[BK][BQ];
+    __shared__ __align__(16) float Cs[BK][BT];
     const int h = blockIdx.z;
     const int dh = D / 2;
     const float *C = h ? C2 : C1;
@@ -36,45 +37,46 @@ __global__ void __launch_bounds__(256) coarse_dots_kernel(const float *__restric
     const int64_t q0 = (int64_t)blockIdx.y * BQ;
     const int t0 = blockIdx.x * BT;
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    float acc[4][4];
+    float acc[8][8];
 #pragma unroll
-    for (int i = 0; i < 4; i++)
+    for (int i = 0; i < 8; i++)
 #pragma unroll
-        for (int j = 0; j < 4; j++) acc[i][j] = 0.f;
-
-    // loader mapping: 256 threads x 4 elements = 64 rows x 16 k
-    const int lr = threadIdx.x >> 2;        // row within tile 0..63
-    const int lk = (threadIdx.x & 3) * 4;   // k offset 0,4,8,12
+        for (int j = 0; j < 8; j++) acc[i][j] = 0.f;
+    // loader: 256 threads x 4 = 128 rows x 8 k (per operand)
+    const int lr = threadIdx.x >> 1;        // row 0..127
+    const int lk = (threadIdx.x & 1) * 4;   // k offset 0 or 4
     for (int k0 = 0; k0 < dh; k0 += BK) {
 #pragma unroll
         for (int u = 0; u < 4; u++) {
-            int kk = k0 + lk + u;
-            int64_t q = q0 + lr;
-            int t = t0 + lr;
+            const int kk = k0 + lk + u;
+            const int64_t q = q0 + lr;
+            const int t = t0 + lr;
             Qs[lk + u][lr] = (q < nq && kk < dh) ? __ldg(Q + q * D + h * dh + kk) : 0.f;
             Cs[lk + u][lr] = (t < T && kk < dh) ? __ldg(C + (int64_t)t * dh + kk) : 0.f;
         }
         __syncthreads();
 #pragma unroll
         for (int kk = 0; kk < BK; kk++) {
-            float4 a = *reinterpret_cast<const float4 *>(&Qs[kk][ty * 4]);
-            float4 b = *reinterpret_cast<const float4 *>(&Cs[kk][tx * 4]);
-            float av[4] = {a.x, a.y, a.z, a.w};
-            float bv[4] = {b.x, b.y, b.z, b.w};
+            const float4 a0 = *reinterpret_cast<const float4 *>(&Qs[kk][ty * 4]);
+            const float4 a1 = *reinterpret_cast<const float4 *>(&Qs[kk][64 + ty * 4]);
+            const float4 b0 = *reinterpret_cast<const float4 *>(&Cs[kk][tx * 4]);
+            const float4 b1 = *reinterpret_cast<const float4 *>(&Cs[kk][64 + tx * 4]);
+            const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
-            for (int i = 0; i < 4; i++)
+            for (int i = 0; i < 8; i++)
 #pragma unroll
-                for (int j = 0; j < 4; j++) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+                for (int j = 0; j < 8; j++) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
         }
         __syncthreads();
     }
 #pragma unroll
-    for (int i = 0; i < 4; i++) {
-        int64_t q = q0 + ty * 4 + i;
+    for (int i = 0; i < 8; i++) {
+        const int64_t q = q0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
         if (q >= nq) continue;
 #pragma unroll
-        for (int j = 0; j < 4; j++) {
-            int t = t0 + tx * 4 + j;
+        for (int j = 0; j < 8; j++) {
+            const int t = t0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
             if (t < T) out[q * T + t] = acc[i][j];
         }
     }
@@ -194,17 +196,24 @@ __global__ void __launch_bounds__(kSortThreads) row_sort_kernel(
     }
 }
 
-// Partial variant for sparse tables: only the P smallest (r, index) of each
-// half in sorted order (plus the unsorted r).  A 4-pass MSB radix select
-// finds the P-th smallest r; elements below it, and the first of its ties in
-// index order, are compacted (index order preserved) and block-sorted.
+// Partial variant for sparse tables: only the smallest P' (256 <= P' <=
+// kTopP when the value spread allows) (r, index) of each half in sorted
+// order, plus the unsorted r.  One 1024-bucket histogram over the block's
+// [min, max] key range (a second, finer one only when the bucket holding
+// rank 256 is overfull) gives a cut value that never splits equal keys;
+// the keys below it are compacted in index order and block-sorted.  P' per
+// (query, half) goes to plen; the traversal queues a query for the
+// full-sort retry pass if it needs a sorted position beyond P'.
+constexpr int kCutMin = 256;
+constexpr int kBuckets = 1024;
+
 template <int ITEMS, int P>
 __global__ void __launch_bounds__(kSortThreads) row_topk_kernel(
     const float *__restrict__ Q, int D, const float *__restrict__ dots1,
     const float *__restrict__ dots2, const float *__restrict__ cn1,
     const float *__restrict__ cn2, int T, float *__restrict__ sr1, float *__restrict__ sr2,
     int32_t *__restrict__ ord1, int32_t *__restrict__ ord2, float *__restrict__ ru1,
-    float *__restrict__ ru2) {
+    float *__restrict__ ru2, int32_t *__restrict__ plen) {
     constexpr int PI = P / kSortThreads;
     using Sort = cub::BlockRadixSort<unsigned int, kSortThreads, PI, int>;
     using Scan = cub::BlockScan<unsigned int, kSortThreads>;
@@ -212,16 +221,18 @@ __global__ void __launch_bounds__(kSortThreads) row_topk_kernel(
         typename Sort::TempStorage sort;
         typename Scan::TempStorage scan;
     } tmp;
-    __shared__ unsigned int hist[256];
+    __shared__ unsigned int hist[kBuckets];
     __shared__ unsigned int skeys[P];
     __shared__ int svals[P];
     __shared__ float s_part[kSortThreads / 32];
+    __shared__ unsigned int s_min[kSortThreads / 32], s_max[kSortThreads / 32];
     __shared__ float s_qn;
-    __shared__ unsigned int s_digit, s_below;
+    __shared__ unsigned int s_lo, s_cut, s_cnt, s_shift;
 
     const int64_t q = blockIdx.x;
     const int h = blockIdx.y;
     const int dh = D / 2;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const float *qv = Q + q * D + h * dh;
     float part = 0.f;
     for (int x = threadIdx.x; x < dh; x += kSortThreads) {
@@ -230,7 +241,7 @@ __global__ void __launch_bounds__(kSortThreads) row_topk_kernel(
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-    if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = part;
+    if (lane == 0) s_part[warp] = part;
     __syncthreads();
     if (threadIdx.x == 0) {
         float sum = 0.f;
@@ -243,6 +254,7 @@ __global__ void __launch_bounds__(kSortThreads) row_topk_kernel(
     const float *cn = h ? cn2 : cn1;
     float *ru = (h ? ru2 : ru1) + q * T;
     unsigned int keys[ITEMS];
+    unsigned int kmin = 0xFFFFFFFFu, kmax = 0u;
 #pragma unroll
     for (int s = 0; s < ITEMS; s++) {
         const int idx = threadIdx.x * ITEMS + s;
@@ -251,79 +263,105 @@ __global__ void __launch_bounds__(kSortThreads) row_topk_kernel(
             if (!(r > 0.f)) r = 0.f;
             keys[s] = __float_as_uint(r);
             ru[idx] = r;
+            kmin = min(kmin, keys[s]);
+            kmax = max(kmax, keys[s]);
         } else {
             keys[s] = 0xFFFFFFFFu;
         }
     }
-    // radix select: value bits of the P-th smallest
-    unsigned int prefix = 0, mask = 0, rank = P;
-    for (int shift = 24; shift >= 0; shift -= 8) {
-        for (int i = threadIdx.x; i < 256; i += kSortThreads) hist[i] = 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+        kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    }
+    if (lane == 0) {
+        s_min[warp] = kmin;
+        s_max[warp] = kmax;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned int a = 0xFFFFFFFFu, b = 0u;
+        for (int w = 0; w < kSortThreads / 32; w++) {
+            a = min(a, s_min[w]);
+            b = max(b, s_max[w]);
+        }
+        const unsigned int range = b - a;
+        const int bits = range ? 32 - __clz(range) : 0;
+        s_lo = a;
+        s_shift = bits > 10 ? bits - 10 : 0;
+        s_cut = 0;
+        s_cnt = 0;
+    }
+    __syncthreads();
+    // up to two histogram refinements of [lo, lo + 1024 << shift)
+    unsigned int below = 0;  // keys already known to be under the window
+    for (int pass = 0; pass < 2; pass++) {
+        const unsigned int lo = s_lo, shift = s_shift;
+        for (int i = threadIdx.x; i < kBuckets; i += kSortThreads) hist[i] = 0;
         __syncthreads();
 #pragma unroll
-        for (int s = 0; s < ITEMS; s++)
-            if (threadIdx.x * ITEMS + s < T && (keys[s] & mask) == prefix) atomicAdd(&hist[(keys[s] >> shift) & 0xFF], 1u);
-        __syncthreads();
-        if (threadIdx.x < 32) {
-            const int lane = threadIdx.x;
-            unsigned int loc[8], sum = 0;
-#pragma unroll
-            for (int x = 0; x < 8; x++) {
-                loc[x] = hist[lane * 8 + x];
-                sum += loc[x];
+        for (int s = 0; s < ITEMS; s++) {
+            if (threadIdx.x * ITEMS + s < T && keys[s] >= lo) {
+                const unsigned int bkt = (keys[s] - lo) >> shift;
+                if (bkt < (unsigned int)kBuckets) atomicAdd(&hist[bkt], 1u);
             }
+        }
+        __syncthreads();
+        if (warp == 0) {
+            // 32 bins per lane
+            unsigned int sum = 0;
+            for (int x = 0; x < kBuckets / 32; x++) sum += hist[lane * (kBuckets / 32) + x];
             unsigned int incl = sum;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 unsigned int y = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += y;
             }
-            unsigned int run = incl - sum;
-#pragma unroll
-            for (int x = 0; x < 8; x++) {
-                if (run < rank && run + loc[x] >= rank) {
-                    s_digit = lane * 8 + x;
-                    s_below = run;
+            unsigned int run = below + incl - sum;
+            for (int x = 0; x < kBuckets / 32; x++) {
+                const int bkt = lane * (kBuckets / 32) + x;
+                const unsigned int c = hist[bkt];
+                if (run < (unsigned int)kCutMin && run + c >= (unsigned int)kCutMin) {
+                    // bucket holding rank kCutMin: cut after it if it fits, else before it
+                    if (run + c <= (unsigned int)P) {
+                        s_cut = lo + ((unsigned int)(bkt + 1) << shift);
+                        s_cnt = run + c;
+                        s_shift = 0xFFFFFFFFu;  // done
+                    } else {
+                        s_cut = lo + ((unsigned int)bkt << shift);
+                        s_cnt = run;
+                        s_lo = lo + ((unsigned int)bkt << shift);  // refine inside this bucket
+                        s_shift = shift > 10 ? shift - 10 : 0;
+                        if (shift == 0) s_shift = 0xFFFFFFFFu;  // single key value: cannot split
+                    }
                 }
-                run += loc[x];
+                run += c;
             }
         }
         __syncthreads();
-        rank -= s_below;
-        prefix |= s_digit << shift;
-        mask |= 0xFFu << shift;
-        __syncthreads();
+        if (s_shift == 0xFFFFFFFFu) break;
+        below = s_cnt;
     }
-    const unsigned int theta = prefix;  // rank = how many of the ties to take
-    unsigned int neq = 0;
-#pragma unroll
-    for (int s = 0; s < ITEMS; s++) neq += (threadIdx.x * ITEMS + s < T && keys[s] == theta) ? 1u : 0u;
-    unsigned int eq_before;
-    Scan(tmp.scan).ExclusiveSum(neq, eq_before);
-    __syncthreads();
+    // (if both passes ended inside an overfull bucket, s_cut / s_cnt hold
+    // the last clean cut below it; a short prefix just retries sooner)
+    const unsigned int cut = s_cut;
     unsigned int take = 0;
-    bool tk[ITEMS];
 #pragma unroll
-    for (int s = 0; s < ITEMS; s++) {
-        const bool valid = threadIdx.x * ITEMS + s < T;
-        bool t = valid && keys[s] < theta;
-        if (valid && keys[s] == theta) {
-            t = eq_before < rank;
-            eq_before++;
-        }
-        tk[s] = t;
-        take += t ? 1u : 0u;
-    }
-    unsigned int pos;
-    Scan(tmp.scan).ExclusiveSum(take, pos);
+    for (int s = 0; s < ITEMS; s++) take += (threadIdx.x * ITEMS + s < T && keys[s] < cut) ? 1u : 0u;
+    unsigned int pos, total;
+    Scan(tmp.scan).ExclusiveSum(take, pos, total);
     __syncthreads();
 #pragma unroll
     for (int s = 0; s < ITEMS; s++) {
-        if (tk[s]) {
+        if (threadIdx.x * ITEMS + s < T && keys[s] < cut) {
             skeys[pos] = keys[s];
             svals[pos] = threadIdx.x * ITEMS + s;
             pos++;
         }
+    }
+    for (int x = total + threadIdx.x; x < P; x += kSortThreads) {
+        skeys[x] = 0xFFFFFFFFu;
+        svals[x] = 0x7FFFFFFF;
     }
     __syncthreads();
     unsigned int k2[PI];
@@ -340,18 +378,21 @@ __global__ void __launch_bounds__(kSortThreads) row_topk_kernel(
 #pragma unroll
     for (int s = 0; s < PI; s++) {
         const int rank_out = s * kSortThreads + threadIdx.x;
-        sr[rank_out] = __uint_as_float(k2[s]);
-        ord[rank_out] = v2[s];
+        if (rank_out < (int)total) {
+            sr[rank_out] = __uint_as_float(k2[s]);
+            ord[rank_out] = v2[s];
+        }
     }
+    if (threadIdx.x == 0) plen[q * 2 + h] = (int32_t)total;
 }
 
 template <int ITEMS>
 int launch_row_topk_t(const float *Q, int64_t nq, int32_t D, const float *dots1, const float *dots2,
                       const float *cn1, const float *cn2, int32_t T, float *sr1, float *sr2, int32_t *ord1,
-                      int32_t *ord2, float *ru1, float *ru2, cudaStream_t stream) {
+                      int32_t *ord2, float *ru1, float *ru2, int32_t *plen, cudaStream_t stream) {
     dim3 grid((unsigned)nq, 2);
     row_topk_kernel<ITEMS, kTopP><<<grid, kSortThreads, 0, stream>>>(Q, D, dots1, dots2, cn1, cn2, T, sr1, sr2,
-                                                                   ord1, ord2, ru1, ru2);
+                                                                   ord1, ord2, ru1, ru2, plen);
     BPQ_CUDA_TRY(cudaGetLastError());
     return BPQ_OK;
 }
@@ -427,16 +468,17 @@ int launch_row_sort(const float *queries, int64_t nq, int32_t D, const float *do
 
 int launch_row_topk(const float *queries, int64_t nq, int32_t D, const float *dots1,
                     const float *dots2, const float *cn1, const float *cn2, int32_t T, float *sr1,
-                    float *sr2, int32_t *ord1, int32_t *ord2, float *ru1, float *ru2, cudaStream_t stream) {
+                    float *sr2, int32_t *ord1, int32_t *ord2, float *ru1, float *ru2, int32_t *plen,
+                    cudaStream_t stream) {
     if (nq == 0) return BPQ_OK;
     if (T <= kSortThreads * 4)
-        return launch_row_topk_t<4>(queries, nq, D, dots1, dots2, cn1, cn2, T, sr1, sr2, ord1, ord2, ru1, ru2, stream);
+        return launch_row_topk_t<4>(queries, nq, D, dots1, dots2, cn1, cn2, T, sr1, sr2, ord1, ord2, ru1, ru2, plen, stream);
     if (T <= kSortThreads * 8)
-        return launch_row_topk_t<8>(queries, nq, D, dots1, dots2, cn1, cn2, T, sr1, sr2, ord1, ord2, ru1, ru2, stream);
+        return launch_row_topk_t<8>(queries, nq, D, dots1, dots2, cn1, cn2, T, sr1, sr2, ord1, ord2, ru1, ru2, plen, stream);
     if (T <= kSortThreads * 16)
-        return launch_row_topk_t<16>(queries, nq, D, dots1, dots2, cn1, cn2, T, sr1, sr2, ord1, ord2, ru1, ru2, stream);
+        return launch_row_topk_t<16>(queries, nq, D, dots1, dots2, cn1, cn2, T, sr1, sr2, ord1, ord2, ru1, ru2, plen, stream);
     if (T <= kSortThreads * 32)
-        return launch_row_topk_t<32>(queries, nq, D, dots1, dots2, cn1, cn2, T, sr1, sr2, ord1, ord2, ru1, ru2, stream);
+        return launch_row_topk_t<32>(queries, nq, D, dots1, dots2, cn1, cn2, T, sr1, sr2, ord1, ord2, ru1, ru2, plen, stream);
     return fail(BPQ_ERR_UNSUPPORTED, "num_coarse > 16384 is outside the row-sort kernel range");
 }
 

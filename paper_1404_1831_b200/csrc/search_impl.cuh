@@ -132,6 +132,7 @@ struct Args {
     const float *dots1, *dots2, *fold;
     const float *ru1, *ru2;          // unsorted half-distances [nq, T] (sparse mode)
     int topP;                        // sorted prefix length available in sr/ord
+    const int32_t *plen;             // per (query, half) prefix length (partial sort) or null
     unsigned int *retry_list, *retry_count;   // queries needing the full sort
     const unsigned int *qlist, *qlist_count;  // indirect query list (retry pass)
     const KT *sr1, *sr2;
@@ -1031,7 +1032,8 @@ struct Query {
     // is queued for the full-sort retry pass).
     __device__ int run_sparse(int4 *band, int4 *pend, int4 *pend2, int4 *other) {
         const unsigned long long L = (unsigned long long)A.L;
-        const bool partial = A.topP < T;
+        const int topP = A.plen ? min(A.plen[qi * 2], A.plen[qi * 2 + 1]) : A.topP;
+        const bool partial = topP < T;
         cw = true;
         unsigned long long W = 0;
         int nr = 0, nc = 0, npend = 0;
@@ -1039,7 +1041,7 @@ struct Query {
         for (;;) {
             // the batch probes rows < nr + NB and columns < nc + NB (column b
             // reads position b + 1): stay inside the sorted prefix
-            if (partial && (nr + NB >= A.topP || nc + NB + 1 >= A.topP)) return 2;
+            if (partial && (nr + NB >= topP || nc + NB + 1 >= topP)) return 2;
             // next NB lines in activation order (merge path over the two sequences)
             if (threadIdx.x < 32) {
                 const int x = warp_first_false(
@@ -1197,7 +1199,7 @@ struct Query {
             const int rs = run_sparse(listA, listB, listC, listD);
             if (rs == 1) return;
             cw = false;
-            if (rs == 2 || A.topP < T) {
+            if (rs == 2 || A.plen != nullptr || A.topP < T) {
                 // needs the full sort: queue for the retry pass (outputs written there)
                 if (threadIdx.x == 0) {
                     S.err = 2;
@@ -1626,6 +1628,7 @@ int launch_one(const Index &ix, const float *queries, int64_t q0, int64_t nq, in
     A.ru1 = ix.rowptr ? ws.ru1 : nullptr;
     A.ru2 = ix.rowptr ? ws.ru2 : nullptr;
     A.topP = ws.topP;
+    A.plen = ws.topP < ix.T ? ws.plen : nullptr;
     A.retry_list = ws.retry_list;
     A.retry_count = ws.retry_count;
     A.qlist = ws.qlist;
