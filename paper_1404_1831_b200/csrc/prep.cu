@@ -214,20 +214,17 @@ __global__ void __launch_bounds__(kSortThreads) row_topk_kernel(
     const float *__restrict__ cn2, int T, float *__restrict__ sr1, float *__restrict__ sr2,
     int32_t *__restrict__ ord1, int32_t *__restrict__ ord2, float *__restrict__ ru1,
     float *__restrict__ ru2, int32_t *__restrict__ plen) {
-    constexpr int PI = P / kSortThreads;
-    using Sort = cub::BlockRadixSort<unsigned int, kSortThreads, PI, int>;
     using Scan = cub::BlockScan<unsigned int, kSortThreads>;
     __shared__ union {
-        typename Sort::TempStorage sort;
         typename Scan::TempStorage scan;
     } tmp;
     __shared__ unsigned int hist[kBuckets];
-    __shared__ unsigned int skeys[P];
-    __shared__ int svals[P];
     __shared__ float s_part[kSortThreads / 32];
     __shared__ unsigned int s_min[kSortThreads / 32], s_max[kSortThreads / 32];
     __shared__ float s_qn;
     __shared__ unsigned int s_lo, s_cut, s_cnt, s_shift;
+    __shared__ unsigned int s_wsum[kSortThreads / 32];
+    __shared__ unsigned long long sk64[P];
 
     const int64_t q = blockIdx.x;
     const int h = blockIdx.y;
@@ -307,20 +304,25 @@ __global__ void __launch_bounds__(kSortThreads) row_topk_kernel(
             }
         }
         __syncthreads();
-        if (warp == 0) {
-            // 32 bins per lane
-            unsigned int sum = 0;
-            for (int x = 0; x < kBuckets / 32; x++) sum += hist[lane * (kBuckets / 32) + x];
-            unsigned int incl = sum;
+        {
+            // all warps: warp w scans bins [64 w, 64 w + 64), 2 per lane
+            constexpr int BPW = kBuckets / (kSortThreads / 32);
+            const int b0 = warp * BPW + lane * 2;
+            const unsigned int c0 = hist[b0], c1 = hist[b0 + 1];
+            unsigned int incl = c0 + c1;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 unsigned int y = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += y;
             }
-            unsigned int run = below + incl - sum;
-            for (int x = 0; x < kBuckets / 32; x++) {
-                const int bkt = lane * (kBuckets / 32) + x;
-                const unsigned int c = hist[bkt];
+            if (lane == 31) s_wsum[warp] = incl;
+            __syncthreads();
+            unsigned int base = below;
+            for (int w = 0; w < warp; w++) base += s_wsum[w];
+            unsigned int run = base + incl - (c0 + c1);
+            for (int x = 0; x < 2; x++) {
+                const int bkt = b0 + x;
+                const unsigned int c = x ? c1 : c0;
                 if (run < (unsigned int)kCutMin && run + c >= (unsigned int)kCutMin) {
                     // bucket holding rank kCutMin: cut after it if it fits, else before it
                     if (run + c <= (unsigned int)P) {
@@ -354,34 +356,37 @@ __global__ void __launch_bounds__(kSortThreads) row_topk_kernel(
 #pragma unroll
     for (int s = 0; s < ITEMS; s++) {
         if (threadIdx.x * ITEMS + s < T && keys[s] < cut) {
-            skeys[pos] = keys[s];
-            svals[pos] = threadIdx.x * ITEMS + s;
+            sk64[pos] = ((unsigned long long)keys[s] << 32) | (unsigned int)(threadIdx.x * ITEMS + s);
             pos++;
         }
     }
-    for (int x = total + threadIdx.x; x < P; x += kSortThreads) {
-        skeys[x] = 0xFFFFFFFFu;
-        svals[x] = 0x7FFFFFFF;
-    }
+    int P2 = 1;
+    while (P2 < (int)total) P2 <<= 1;
+    for (int x = total + threadIdx.x; x < P2; x += kSortThreads) sk64[x] = ~0ull;
     __syncthreads();
-    unsigned int k2[PI];
-    int v2[PI];
-#pragma unroll
-    for (int s = 0; s < PI; s++) {
-        k2[s] = skeys[threadIdx.x * PI + s];
-        v2[s] = svals[threadIdx.x * PI + s];
+    // bitonic sort of (value, index): equal values keep ascending index (stable)
+    for (int k = 2; k <= P2; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < P2; i += kSortThreads) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const bool up = (i & k) == 0;
+                    const unsigned long long x = sk64[i], y = sk64[ixj];
+                    if ((x > y) == up) {
+                        sk64[i] = y;
+                        sk64[ixj] = x;
+                    }
+                }
+            }
+            __syncthreads();
+        }
     }
-    __syncthreads();
-    Sort(tmp.sort).SortBlockedToStriped(k2, v2, 0, 32);
     float *sr = (h ? sr2 : sr1) + q * T;
     int32_t *ord = (h ? ord2 : ord1) + q * T;
-#pragma unroll
-    for (int s = 0; s < PI; s++) {
-        const int rank_out = s * kSortThreads + threadIdx.x;
-        if (rank_out < (int)total) {
-            sr[rank_out] = __uint_as_float(k2[s]);
-            ord[rank_out] = v2[s];
-        }
+    for (int x = threadIdx.x; x < (int)total; x += kSortThreads) {
+        const unsigned long long kv = sk64[x];
+        sr[x] = __uint_as_float((unsigned int)(kv >> 32));
+        ord[x] = (int32_t)(kv & 0xFFFFFFFFu);
     }
     if (threadIdx.x == 0) plen[q * 2 + h] = (int32_t)total;
 }
