@@ -29,11 +29,14 @@ int fail(int code, const std::string &msg);
 // Tunables of the fused traversal + scan + top-k kernel.
 constexpr int kSearchThreads = 256;     // threads per CTA (one CTA per query at a time)
 constexpr int kTopkBuf = 2048;          // per-CTA top-k candidate buffer (u64 keys)
-constexpr int kMaxK = kTopkBuf - 4 * kSearchThreads;  // largest k the engine accepts
+constexpr int kMaxK = 1024;             // largest k the engine accepts
 constexpr int kSortCap = 512;           // final-band cells sorted in shared memory
 constexpr int kTopP = 1024;             // sorted prefix per half for sparse-table queries
 constexpr int kMultiLines = 8;          // lines a warp evaluates per threshold in a multi-probe round
-constexpr int kLutMin = 96;             // cells with >= this many entries are scanned via a smem LUT
+#ifndef BPQ_LUT_MIN
+#define BPQ_LUT_MIN 256
+#endif
+constexpr int kLutMin = BPQ_LUT_MIN;    // cells with >= this many entries are scanned via a smem LUT
 constexpr int kBandCap = 32768;         // max cells enumerated per band
 constexpr int kMaxDim = 1024;           // queries staged in shared memory
 

@@ -93,6 +93,8 @@ struct __align__(16) Smem {
     uint32_t tcnt;
     unsigned long long tsel_below;
     unsigned long long tkey;
+    uint32_t nholes;
+    uint16_t holes[kMaxK];
 };
 
 #ifdef BPQ_PHASE_PROF
@@ -416,20 +418,20 @@ __device__ void topk_compact(Smem &S, int k) {
         __syncthreads();
     }
     const unsigned long long kth = prefix;
-    // compact keys <= kth (exactly k of them) to the front
-    unsigned long long keep[kTopkBuf / NT];
-    int nk = 0;
-#pragma unroll
-    for (int x = 0; x < kTopkBuf / NT; x++) {
-        const uint32_t i = threadIdx.x + x * NT;
-        if (i < n && S.tk[i] <= kth) keep[nk++] = S.tk[i];
+    // move the survivors (keys <= kth, exactly k of them) into [0, k): slots
+    // below k holding larger keys are holes, survivors at or above k fill them
+    if (threadIdx.x == 0) {
+        S.tcnt = 0;
+        S.nholes = 0;
     }
-    if (threadIdx.x == 0) S.tcnt = 0;
     __syncthreads();
-    uint32_t base = nk ? atomicAdd(&S.tcnt, (uint32_t)nk) : 0;
-#pragma unroll
-    for (int x = 0; x < kTopkBuf / NT; x++)
-        if (x < nk) S.tk[base + x] = keep[x];
+    for (int i = threadIdx.x; i < k; i += NT)
+        if (S.tk[i] > kth) S.holes[atomicAdd(&S.nholes, 1u)] = (uint16_t)i;
+    __syncthreads();
+    for (uint32_t i = k + threadIdx.x; i < n; i += NT) {
+        const unsigned long long key = S.tk[i];
+        if (key <= kth) S.tk[S.holes[atomicAdd(&S.tcnt, 1u)]] = key;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         S.ntk = (uint32_t)k;
@@ -560,6 +562,8 @@ struct Query {
             lut[idx] = __fadd_rn(tab[idx], __fmul_rn(2.f, x));
         }
         __syncthreads();
+        // Rounds need no block barrier while the top-k buffer has room for
+        // every key they could insert: sync (and compact) only between segments.
         for (uint32_t e0 = 0; e0 < lc; e0 += NT * kUnroll) {
             uint32_t w[kUnroll][4];
             uint32_t idv[kUnroll];
