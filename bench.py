@@ -50,6 +50,11 @@ CONFIGS = {
                engine="fbpq", train=262_144),
     "c2": dict(n=10_000_000, dim=128, ncomp=4096, t=4096, m=8, k=256, nq=10_000, L=10_000, topk=100,
                engine="hbpq", train=262_144),
+    # billion-scale (BASELINE configs[4]) on one GPU: streamed build, 16,384 components
+    "c4": dict(n=1_000_000_000, dim=128, ncomp=16384, t=16384, m=8, k=256, nq=10_000, L=10_000, topk=100,
+               engine="fbpq", train=1_048_576, stream=True),
+    "c4m16": dict(n=1_000_000_000, dim=128, ncomp=16384, t=16384, m=16, k=256, nq=10_000, L=10_000, topk=100,
+                  engine="fbpq", train=1_048_576, stream=True),
     "c1small": dict(n=1_000_000, dim=128, ncomp=4096, t=1024, m=8, k=256, nq=10_000, L=10_000, topk=100,
                     engine="fbpq", train=131_072),
 }
@@ -72,7 +77,7 @@ def build_workload(cfg, device, rank=0):
         q = torch.from_numpy(g["queries"].astype(np.float32)).to(device)
         host = dict(c1=g["c1"], c2=g["c2"], offsets=g["offsets"], ids=g["ids"], codes=g["codes"], books=g["books"],
                     tables=tables)
-        return dix, q, host
+        return dix, q, (lambda: host)
     t0 = time.time()
     cent = datagen.mixture_centres(cfg["ncomp"], cfg["dim"])
     train = datagen.clipped_mixture_torch(cfg["train"], cfg["dim"], cfg["ncomp"], datagen.SEED_TRAIN, device, cent)
@@ -87,8 +92,19 @@ def build_workload(cfg, device, rank=0):
     books = np.stack([encode.train_kmeans(disp[:, p * ds:(p + 1) * ds].contiguous(), cfg["k"], iters=8, seed=20 + p)
                       for p in range(cfg["m"])])
     log(f"[setup] codebooks trained in {time.time() - t0:.1f}s")
-    base = datagen.clipped_mixture_torch(cfg["n"], cfg["dim"], cfg["ncomp"], datagen.SEED_BASE, device, cent)
-    if cfg["engine"] == "hbpq":
+    if cfg.get("stream"):
+        centt = torch.as_tensor(cent, dtype=torch.float32, device=device)
+        dix = encode.build_index_streamed(
+            cfg["n"], lambda s, e: datagen.clipped_mixture_chunk(s, e, cfg["dim"], cfg["ncomp"], datagen.SEED_BASE,
+                                                                 device, centt),
+            c1, c2, books, device=device)
+        host_books = dict(books=books)
+        base = None
+    else:
+        base = datagen.clipped_mixture_torch(cfg["n"], cfg["dim"], cfg["ncomp"], datagen.SEED_BASE, device, cent)
+    if cfg.get("stream"):
+        pass
+    elif cfg["engine"] == "hbpq":
         # local books per half-codeword: pooled residual books + per-row perturbation
         # (bank training is out of scope; codes are encoded against these books)
         m2 = cfg["m"] // 2
@@ -108,11 +124,15 @@ def build_workload(cfg, device, rank=0):
                                       device, cent)
     log(f"[setup] index built in {time.time() - t0:.1f}s: N={dix.n} populated="
         f"{int((torch.diff(dix.offsets.long() & 0xFFFFFFFF) > 0).sum())}")
-    host = dict(c1=c1, c2=c2, offsets=(dix.offsets.cpu().numpy().view(np.uint32)).astype(np.int64),
-                ids=dix.ids.cpu().numpy().view(np.uint32), codes=dix.codes.cpu().numpy(), **host_books)
-    if cfg["engine"] != "hbpq":
-        host["tables"] = (dix.cn1.cpu().numpy(), dix.cn2.cpu().numpy(), dix.fine_norms.cpu().numpy(),
-                          dix.cross1.cpu().numpy(), dix.cross2.cpu().numpy())
+    def host():
+        """Host copy of the index for the CPU baseline (built on demand)."""
+        h = dict(c1=c1, c2=c2, offsets=(dix.offsets.cpu().numpy().view(np.uint32)).astype(np.int64),
+                 ids=dix.ids.cpu().numpy().view(np.uint32), codes=dix.codes.cpu().numpy(), **host_books)
+        if cfg["engine"] != "hbpq":
+            h["tables"] = (dix.cn1.cpu().numpy(), dix.cn2.cpu().numpy(), dix.fine_norms.cpu().numpy(),
+                           dix.cross1.cpu().numpy(), dix.cross2.cpu().numpy())
+        return h
+
     return dix, q, host
 
 
@@ -194,6 +214,16 @@ def cpu_baseline(host, engine, queries_np, L, k, budget_s=20.0):
             "codes_per_s": float(nc.sum()) / dt}
 
 
+def launches_per_step(dix, engine):
+    """Engine kernels per bpq_search call (one query chunk): first layer, row
+    sort (partial on sparse tables), fold (FBPQ), fused search, and the
+    full-sort + search retry pass after a partial sort."""
+    n = 3 + (1 if engine == "fbpq" else 0)
+    if dix.row_ptr is not None and dix.t > 1024:
+        n += 2
+    return n
+
+
 # ------------------------------------------------------------------------ run
 def main():
     ap = argparse.ArgumentParser()
@@ -249,11 +279,12 @@ def main():
 
     if args.impl == "reference":
         qn = q.cpu().numpy()
+        hostd = host()
         steps_v = []
         for s in range(args.warmup + args.steps):
             per = max(1, 64 // 1)
             lo = (s * per) % max(1, nq - per)
-            dt, nc = cpu_search(host, engine, qn[lo:lo + per], L, k, os.cpu_count())
+            dt, nc = cpu_search(hostd, engine, qn[lo:lo + per], L, k, os.cpu_count())
             if s >= args.warmup:
                 steps_v.append((per, dt, float(nc.sum())))
         tot_q = sum(x[0] for x in steps_v)
@@ -372,12 +403,12 @@ def main():
                      "peak_source": HBM_PEAK_SRC, "alg_bytes_per_launch": alg_bytes},
         "e2e": {"value": e2e_v, "unit": "queries/s", "h2d_bytes_per_step": int(q.numel() * 4),
                 "d2h_bytes_per_step": int(nq * k * 8 + nq * 4)},
-        "gpu_launches": 3 * args.steps,
+        "gpu_launches": launches_per_step(dix, engine) * args.steps,
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            line["cpu_baseline"] = cpu_baseline(host, engine, q.cpu().numpy(), L, k)
+            line["cpu_baseline"] = cpu_baseline(host(), engine, q.cpu().numpy(), L, k)
         except Exception as e:  # the baseline is reported, never required
             line["cpu_baseline"] = {"error": repr(e)}
     if rank == 0:

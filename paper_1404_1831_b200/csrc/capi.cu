@@ -27,9 +27,9 @@ struct SearchLayout {
 };
 
 int64_t query_chunk(int64_t nq, int32_t T, int32_t M, int32_t K) {
-    // keep the per-chunk first-layer buffers (10 arrays of [chunk, T] x 4 B + fold) near 2 GiB
+    // keep the per-chunk first-layer buffers (10 arrays of [chunk, T] x 4 B + fold) near 8 GiB
     int64_t per_q = (int64_t)T * 40 + (int64_t)M * K * 4 + 4;
-    int64_t c = ((int64_t)2 << 30) / per_q;
+    int64_t c = ((int64_t)8 << 30) / per_q;
     c = std::max<int64_t>(c, 256);
     return std::max<int64_t>(1, std::min<int64_t>(nq, c));
 }

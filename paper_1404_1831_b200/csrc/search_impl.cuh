@@ -537,9 +537,17 @@ struct Query {
         }
     }
 
-    __device__ __forceinline__ void round_end() {
+    // Offer with the id loaded only when the distance can enter the top-k
+    // (dist bits <= threshold's): most candidates are rejected on the
+    // distance alone, which saves the id read (4 of the 12 B per candidate).
+    __device__ __forceinline__ void offer_lazy(float dist, const uint32_t *idp) {
+        const uint32_t db = canon_bits(dist);
+        if (db <= (uint32_t)(S.thr >> 32)) offer(dist, __ldg(idp));
+    }
+
+    __device__ __forceinline__ void round_end(int cap = NT * kUnroll) {
         __syncthreads();
-        if (S.ntk > (uint32_t)(kTopkBuf - NT * kUnroll)) {
+        if (S.ntk > (uint32_t)(kTopkBuf - cap)) {
             const int pv = PROF(PH_COMPACT);
             topk_compact(S, A.k);
             PROF(pv);
@@ -562,31 +570,26 @@ struct Query {
             lut[idx] = __fadd_rn(tab[idx], __fmul_rn(2.f, x));
         }
         __syncthreads();
-        // Rounds need no block barrier while the top-k buffer has room for
-        // every key they could insert: sync (and compact) only between segments.
-        for (uint32_t e0 = 0; e0 < lc; e0 += NT * kUnroll) {
-            uint32_t w[kUnroll][4];
-            uint32_t idv[kUnroll];
+        // kLutUnroll codes per thread per round keep 2x the bytes in flight
+        for (uint32_t e0 = 0; e0 < lc; e0 += NT * kLutUnroll) {
+            uint32_t w[kLutUnroll][4];
 #pragma unroll
-            for (int u = 0; u < kUnroll; u++) {
+            for (int u = 0; u < kLutUnroll; u++) {
                 const uint32_t e = e0 + u * NT + threadIdx.x;
-                if (e < lc) {
-                    load_code<MT>(A.codes + (size_t)(lst + e) * M, w[u], M);
-                    idv[u] = __ldg(A.ids + lst + e);
-                }
+                if (e < lc) load_code<MT>(A.codes + (size_t)(lst + e) * M, w[u], M);
             }
 #pragma unroll
-            for (int u = 0; u < kUnroll; u++) {
+            for (int u = 0; u < kLutUnroll; u++) {
                 const uint32_t e = e0 + u * NT + threadIdx.x;
                 if (e < lc) {
                     float acc = cb;
 #pragma unroll
                     for (int p = 0; p < M; p++) acc = __fadd_rn(acc, lut[p * K + code_at(w[u], p)]);
                     if (acc < 0.f) acc = 0.f;
-                    offer(acc, idv[u]);
+                    offer_lazy(acc, A.ids + lst + e);
                 }
             }
-            round_end();
+            round_end(NT * kLutUnroll);
         }
         __syncthreads();
         PROF(pv);
@@ -647,7 +650,6 @@ struct Query {
                     uint32_t entry[kUnroll];
                     int own[kUnroll];
                     uint32_t w[kUnroll][4];
-                    uint32_t idv[kUnroll];
 #pragma unroll
                     for (int u = 0; u < kUnroll; u++) {
                         const uint32_t e = e0 + u * NT + threadIdx.x;
@@ -661,7 +663,6 @@ struct Query {
                             own[u] = lo;
                             entry[u] = S.cstart[lo] + (e - S.cpre[lo]);
                             load_code<MT>(A.codes + (size_t)entry[u] * M, w[u], M);
-                            idv[u] = __ldg(A.ids + entry[u]);
                         }
                     }
 #pragma unroll
@@ -673,7 +674,7 @@ struct Query {
                             dist = dist_fbpq<MT>(A, tab, S.coi[lo], S.coj[lo], S.cbase[lo], w[u]);
                         else
                             dist = dist_recon<ENGINE, MT>(A, tab, S.coi[lo], S.coj[lo], w[u]);
-                        offer(dist, idv[u]);
+                        offer_lazy(dist, A.ids + entry[u]);
                     }
                     round_end();
                 }

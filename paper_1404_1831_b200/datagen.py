@@ -55,6 +55,27 @@ def clipped_mixture_torch(n: int, dim: int, ncomp: int, seed: int, device, centr
     return out
 
 
+def clipped_mixture_chunk(s: int, e: int, dim: int, ncomp: int, seed: int, device, cent=None):
+    """Rows [s, e) of a streamed clipped-mixture database: each 2^20-row
+    block has its own seeded generator, so any row range is reproducible
+    without generating the rows before it."""
+    import torch
+
+    if cent is None:
+        cent = torch.as_tensor(mixture_centres(ncomp, dim), dtype=torch.float32, device=device)
+    out = torch.empty((e - s, dim), dtype=torch.float32, device=device)
+    blk = 1 << 20
+    g = torch.Generator(device=device)
+    for b0 in range((s // blk) * blk, e, blk):
+        g.manual_seed(1_000_003 * seed + 7919 * (b0 // blk) + 17)
+        j = torch.randint(0, ncomp, (blk,), generator=g, device=device)
+        z = torch.randn((blk, dim), generator=g, device=device)
+        lo, hi = max(s, b0), min(e, b0 + blk)
+        sl = slice(lo - b0, hi - b0)
+        out[lo - s : hi - s] = torch.clamp(torch.round(cent[j[sl]] + 20.0 * z[sl]), 0, 255)
+    return out
+
+
 def normalized_mixture_torch(n: int, dim: int, ncomp: int, seed: int, device, sigma=0.3, chunk=1 << 22):
     import torch
 

@@ -146,6 +146,40 @@ def build_index(base, c1, c2, books, id_offset=0, *, tables=None, device=None):
                        tables=tables, device=dev)
 
 
+def build_index_streamed(n, make_chunk, c1, c2, books, id_offset=0, *, chunk=1 << 24, tables=None, device=None):
+    """build_index for databases that do not fit the device as f32: rows
+    [s, e) come from make_chunk(s, e) (a device f32 tensor), are assigned and
+    encoded chunk by chunk, and only (i, j, codes) are kept for the packing."""
+    import torch
+
+    dev = torch.device(device or "cuda")
+    c1n = np.asarray(c1, np.float32)
+    c2n = np.asarray(c2, np.float32)
+    booksn = np.asarray(books, np.float32)
+    t = c1n.shape[0]
+    m = booksn.shape[0]
+    _check_fine_params(2 * c1n.shape[1], m, booksn.shape[1])
+    i_all = torch.empty(n, dtype=torch.int64, device=dev)
+    j_all = torch.empty(n, dtype=torch.int64, device=dev)
+    codes = torch.empty((n, m), dtype=torch.uint8, device=dev)
+    cn1, cn2 = coarse_norms(c1n), coarse_norms(c2n)
+    for s in range(0, n, chunk):
+        e = min(n, s + chunk)
+        x = make_chunk(s, e)
+        i, j = assign_cells(x, c1n, c2n, cn1=cn1, cn2=cn2)
+        i_all[s:e] = i
+        j_all[s:e] = j
+        codes[s:e] = encode_residual(x, i, j, c1n, c2n, booksn)
+        del x, i, j
+    offsets, ids, pcodes = pack_cells(i_all, j_all, codes, t, id_offset)
+    del i_all, j_all, codes
+    torch.cuda.empty_cache()
+    if tables is None:
+        tables = build_tables_host(c1n, c2n, booksn)
+    return DeviceIndex(c1=c1n, c2=c2n, offsets=offsets, ids=ids, codes=pcodes, books=booksn,
+                       tables=tables, device=dev)
+
+
 def build_hbpq_index(base, c1, c2, bank1, bank2, id_offset=0, *, device=None):
     """build_hbpq_index (hbpq.py:293-313) on the device."""
     import torch
