@@ -55,6 +55,9 @@ CONFIGS = {
                engine="fbpq", train=1_048_576, stream=True),
     "c4m16": dict(n=1_000_000_000, dim=128, ncomp=16384, t=16384, m=16, k=256, nq=10_000, L=10_000, topk=100,
                   engine="fbpq", train=1_048_576, stream=True),
+    # higher-dimensional dense features (BASELINE configs[3]) on one GPU
+    "c3": dict(n=50_000_000, dim=384, ncomp=4096, t=4096, m=16, k=256, nq=10_000, L=30_000, topk=100,
+               engine="fbpq", train=524_288, stream=True, normalized=True),
     "c1small": dict(n=1_000_000, dim=128, ncomp=4096, t=1024, m=8, k=256, nq=10_000, L=10_000, topk=100,
                     engine="fbpq", train=131_072),
 }
@@ -79,8 +82,21 @@ def build_workload(cfg, device, rank=0):
                     tables=tables)
         return dix, q, (lambda: host)
     t0 = time.time()
-    cent = datagen.mixture_centres(cfg["ncomp"], cfg["dim"])
-    train = datagen.clipped_mixture_torch(cfg["train"], cfg["dim"], cfg["ncomp"], datagen.SEED_TRAIN, device, cent)
+    if cfg.get("normalized"):
+        centt = datagen.normalized_centres_torch(cfg["ncomp"], cfg["dim"], device)
+
+        def draw(s, e, seed):
+            return datagen.normalized_mixture_chunk(s, e, cfg["dim"], cfg["ncomp"], seed, device, centt)
+    else:
+        cent = datagen.mixture_centres(cfg["ncomp"], cfg["dim"])
+        centt = torch.as_tensor(cent, dtype=torch.float32, device=device)
+
+        def draw(s, e, seed):
+            return datagen.clipped_mixture_chunk(s, e, cfg["dim"], cfg["ncomp"], seed, device, centt)
+    if cfg.get("stream"):
+        train = draw(0, cfg["train"], datagen.SEED_TRAIN)
+    else:
+        train = datagen.clipped_mixture_torch(cfg["train"], cfg["dim"], cfg["ncomp"], datagen.SEED_TRAIN, device, cent)
     dh = cfg["dim"] // 2
     c1 = encode.train_kmeans(train[:, :dh].contiguous(), cfg["t"], iters=8, seed=11)
     c2 = encode.train_kmeans(train[:, dh:].contiguous(), cfg["t"], iters=8, seed=12)
@@ -93,11 +109,8 @@ def build_workload(cfg, device, rank=0):
                       for p in range(cfg["m"])])
     log(f"[setup] codebooks trained in {time.time() - t0:.1f}s")
     if cfg.get("stream"):
-        centt = torch.as_tensor(cent, dtype=torch.float32, device=device)
-        dix = encode.build_index_streamed(
-            cfg["n"], lambda s, e: datagen.clipped_mixture_chunk(s, e, cfg["dim"], cfg["ncomp"], datagen.SEED_BASE,
-                                                                 device, centt),
-            c1, c2, books, device=device)
+        dix = encode.build_index_streamed(cfg["n"], lambda s, e: draw(s, e, datagen.SEED_BASE), c1, c2, books,
+                                          device=device)
         host_books = dict(books=books)
         base = None
     else:
@@ -120,8 +133,11 @@ def build_workload(cfg, device, rank=0):
         host_books = dict(books=books)
     del base
     torch.cuda.empty_cache()
-    q = datagen.clipped_mixture_torch(cfg["nq"], cfg["dim"], cfg["ncomp"], datagen.SEED_QUERIES + 1000 * rank,
-                                      device, cent)
+    if cfg.get("stream"):
+        q = draw(0, cfg["nq"], datagen.SEED_QUERIES + 1000 * rank)
+    else:
+        q = datagen.clipped_mixture_torch(cfg["nq"], cfg["dim"], cfg["ncomp"], datagen.SEED_QUERIES + 1000 * rank,
+                                          device, cent)
     log(f"[setup] index built in {time.time() - t0:.1f}s: N={dix.n} populated="
         f"{int((torch.diff(dix.offsets.long() & 0xFFFFFFFF) > 0).sum())}")
     def host():

@@ -91,3 +91,30 @@ def normalized_mixture_torch(n: int, dim: int, ncomp: int, seed: int, device, si
         x = cent[j] + sigma * torch.randn((e - s, dim), generator=g, device=device)
         out[s:e] = x / torch.linalg.vector_norm(x, dim=1, keepdim=True)
     return out
+
+
+def normalized_centres_torch(ncomp: int, dim: int, device, seed: int = SEED_CENTRES):
+    import torch
+
+    gc = torch.Generator(device=device)
+    gc.manual_seed(seed + 7)
+    return torch.randn((ncomp, dim), generator=gc, device=device)
+
+
+def normalized_mixture_chunk(s: int, e: int, dim: int, ncomp: int, seed: int, device, cent, sigma=0.3):
+    """Rows [s, e) of the config-3 database (centres N(0, I), within-component
+    sigma, then L2-normalised), reproducible per 2^20-row block."""
+    import torch
+
+    out = torch.empty((e - s, dim), dtype=torch.float32, device=device)
+    blk = 1 << 20
+    g = torch.Generator(device=device)
+    for b0 in range((s // blk) * blk, e, blk):
+        g.manual_seed(1_000_003 * seed + 7919 * (b0 // blk) + 29)
+        j = torch.randint(0, ncomp, (blk,), generator=g, device=device)
+        z = torch.randn((blk, dim), generator=g, device=device)
+        lo, hi = max(s, b0), min(e, b0 + blk)
+        sl = slice(lo - b0, hi - b0)
+        x = cent[j[sl]] + sigma * z[sl]
+        out[lo - s : hi - s] = x / torch.linalg.vector_norm(x, dim=1, keepdim=True)
+    return out

@@ -10,3 +10,5 @@ run --config c0 --engine baseline
 for L in 1000 10000 100000; do for k in 1 10 100; do run --config c1 --L $L --k $k; done; done
 run --config c1 --engine baseline
 run --config c2
+run --config c3
+run --config c4

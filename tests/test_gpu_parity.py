@@ -284,3 +284,64 @@ def test_device_encoding_matches_reference(c0, torch_cuda):
     assert np.mean(ids == c0["enc_ids"]) > 0.99
     assert np.mean(np.all(codes == c0["enc_codes"], axis=1)) > 0.99
     assert off[-1] == x.shape[0] and np.all(np.diff(off) >= 0)
+
+
+@pytest.mark.parametrize("engine", ["fbpq", "baseline"])
+def test_m16_high_dim_normalized_vs_oracle(torch_cuda, oracle, engine):
+    """M=16 codes (uint4 loads), D=96 L2-normalised data (config-3 style, no
+    integer structure), dense and sparse traversal."""
+    from paper_1404_1831_b200 import DeviceIndex
+
+    rng = np.random.default_rng(21)
+    t, dim, m, kk, n = 48, 96, 16, 32, 8000
+    cent = rng.normal(size=(64, dim)).astype(np.float32)
+    x = cent[rng.integers(0, 64, n)] + 0.3 * rng.normal(size=(n, dim))
+    base = (x / np.linalg.norm(x, axis=1, keepdims=True)).astype(np.float32)
+    c1 = base[rng.choice(n, t, replace=False), : dim // 2].copy()
+    c2 = base[rng.choice(n, t, replace=False), dim // 2 :].copy()
+    books = (0.05 * rng.normal(size=(m, kk, dim // m))).astype(np.float32)
+    off, ids, codes = oracle.build_index(base, c1, c2, books)
+    idx = oracle.Index(c1, c2, off, ids, codes, books=books)
+    xq = cent[rng.integers(0, 64, 40)] + 0.3 * rng.normal(size=(40, dim))
+    q = (xq / np.linalg.norm(xq, axis=1, keepdims=True)).astype(np.float32)
+    for lists in (False, True):
+        dix = DeviceIndex(c1=c1, c2=c2, offsets=off, ids=ids, codes=codes, books=books, tables=idx.tables,
+                          cell_lists=lists)
+        for L, k in ((50, 10), (1500, 100)):
+            wd, wi, wc, _ = oracle.search_batch_numpy(idx, engine, q, L, k)
+            d, i, c = dix.search(q, L, k, engine).numpy()
+            check_topk(d, i, c, wd, wi, wc, _qn(q), min_exact_frac=0.85)
+
+
+def test_scale_sparse_index_vs_oracle(torch_cuda, oracle):
+    """A 1M-point index from the BASELINE clipped-mixture generator (T=1024,
+    sparse cell table, partial sort + retry in play) against the C oracle."""
+    import torch
+
+    from paper_1404_1831_b200 import DeviceIndex, datagen, encode
+
+    dev = torch.device("cuda")
+    cent = datagen.mixture_centres(1024, 128)
+    train = datagen.clipped_mixture_torch(131_072, 128, 1024, datagen.SEED_TRAIN, dev, cent)
+    c1 = encode.train_kmeans(train[:, :64].contiguous(), 1024, iters=6, seed=1)
+    c2 = encode.train_kmeans(train[:, 64:].contiguous(), 1024, iters=6, seed=2)
+    i, j = encode.assign_cells(train, c1, c2)
+    disp = train - torch.cat([torch.from_numpy(c1).to(dev)[i], torch.from_numpy(c2).to(dev)[j]], 1)
+    books = np.stack([encode.train_kmeans(disp[:, p * 16:(p + 1) * 16].contiguous(), 256, iters=4, seed=10 + p)
+                      for p in range(8)])
+    base = datagen.clipped_mixture_torch(1_000_000, 128, 1024, datagen.SEED_BASE, dev, cent)
+    dix = encode.build_index(base, c1, c2, books)
+    assert dix.row_ptr is not None
+    q = datagen.clipped_mixture_torch(256, 128, 1024, datagen.SEED_QUERIES, dev, cent).cpu().numpy()
+    off = dix.offsets.cpu().numpy().view(np.uint32).astype(np.int64)
+    idx = oracle.Index(c1, c2, off, dix.ids.cpu().numpy().view(np.uint32), dix.codes.cpu().numpy(), books=books,
+                       tables=(dix.cn1.cpu().numpy(), dix.cn2.cpu().numpy(), dix.fine_norms.cpu().numpy(),
+                               dix.cross1.cpu().numpy(), dix.cross2.cpu().numpy()))
+    for L, k in ((1000, 10), (10_000, 100), (100_000, 100)):
+        res = dix.search(q, L, k, "fbpq", ncand=True)
+        d, i_, c = res.numpy()
+        # properties on all queries: sorted, counts, candidates >= L (budget semantics)
+        assert (np.diff(d, axis=1)[:, : k - 1][c[:, None] > np.arange(1, k)[None, :]] >= 0).all()
+        assert (res.ncand.cpu().numpy() >= min(L, 1_000_000)).all()
+        wd, wi, wc, wn = oracle.search_batch_c(idx, "fbpq", q[:48], L, k, threads=8)
+        check_topk(d[:48], i_[:48], c[:48], wd, wi, wc, _qn(q[:48]), min_exact_frac=0.9)
