@@ -50,7 +50,7 @@ constexpr int NT = kSearchThreads;
 constexpr int NW = NT / 32;
 constexpr int ENGINE_TRAVERSE = 3;
 #ifndef BPQ_MINB
-#define BPQ_MINB 3
+#define BPQ_MINB 4
 #endif
 constexpr int kUnroll = 4;                // candidates per thread per round
 constexpr int kSrSmem = 4096;             // sorted half-distances staged in smem
