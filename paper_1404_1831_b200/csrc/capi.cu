@@ -1,5 +1,6 @@
 // C ABI: index lifecycle, batched search orchestration, traversal stage.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -273,7 +274,8 @@ extern "C" int bpq_search_ex(const bpq_index *index, int engine, const float *qu
         // sparse tables only need the activated lines' sorted prefix: partial
         // sort first, full sort only for queries that outgrow it (retry pass)
         const bool sparse = ix.rowptr != nullptr;
-        const bool partial = sparse && ix.T > kTopP && out_popped == nullptr;
+        static const bool force_full = getenv("BPQ_FORCE_FULL_SORT") != nullptr;  // diagnostics
+        const bool partial = sparse && ix.T > kTopP && out_popped == nullptr && !force_full;
         if (partial) {
             rc = launch_row_topk(qc, n, ix.D, ws.dots1, ws.dots2, ix.cn1, ix.cn2, ix.T, ws.sr1, ws.sr2,
                                  ws.ord1, ws.ord2, ws.ru1, ws.ru2, ws.plen, s);

@@ -111,7 +111,7 @@ __device__ __forceinline__ int prof_switch(Smem &S, unsigned long long *acc, int
 }
 #define PROF(ph) prof_switch(S, A.prof, (ph))
 #else
-#define PROF(ph) 0
+#define PROF(ph) ((void)0, 0)
 #endif
 
 // Optional per-phase cycle accounting (compile with -DBPQ_PHASE_PROF): thread 0
@@ -465,6 +465,7 @@ struct Query {
     const float *u1, *u2;    // unsorted half-distances (codeword-keyed entries)
     bool cw;                 // list entries hold codewords (i, j) instead of positions (a, b)
     int T, P, M;
+    int tp1, tp2;              // valid sorted prefix per half (partial sort), block-uniform
     unsigned long long ncand;  // uniform across the CTA
     unsigned long long popped;
 
@@ -489,12 +490,13 @@ struct Query {
         popped = 0;
     }
 
-    __device__ __forceinline__ double k1(int a) const { return a < P ? (double)s1s[a] : (double)__ldg(sr1 + a); }
-    __device__ __forceinline__ double k2(int b) const { return b < P ? (double)s2s[b] : (double)__ldg(sr2 + b); }
+    // plain (not read-only-path) loads: extend() appends to sr/ord in-kernel
+    __device__ __forceinline__ double k1(int a) const { return a < P ? (double)s1s[a] : (double)sr1[a]; }
+    __device__ __forceinline__ double k2(int b) const { return b < P ? (double)s2s[b] : (double)sr2[b]; }
     __device__ __forceinline__ double key(int a, int b) const { return k1(a) + k2(b); }
 
     __device__ __forceinline__ unsigned long long lin_of(int a, int b) const {
-        return (unsigned long long)__ldg(o1 + a) * (unsigned long long)T + (unsigned)__ldg(o2 + b);
+        return (unsigned long long)o1[a] * (unsigned long long)T + (unsigned)o2[b];
     }
 
     // List entries: x = (hi << 16) | lo, positions (a, b) in the band
@@ -514,8 +516,8 @@ struct Query {
             oi = x;
             oj = y;
         } else {
-            oi = __ldg(o1 + x);
-            oj = __ldg(o2 + y);
+            oi = o1[x];
+            oj = o2[y];
         }
     }
 
@@ -1028,6 +1030,74 @@ struct Query {
     // selected inside them.  No threshold search and no empty cell is ever
     // touched.  Returns false (nothing emitted) if the pool would overflow;
     // the caller then falls back to the band traversal.
+    // Lazily extend half h's sorted prefix to at least `need` positions: the
+    // next E smallest (r bits, codeword) keys after the current last one are
+    // found by an MSB radix select over the unsorted r, bitonic-sorted in
+    // shared memory and appended to sr/ord.  Only queries whose traversal
+    // outgrows the partial sort pay for it.
+    __device__ void extend(int h, int need) {
+        int tp = h ? tp2 : tp1;
+        const float *u = h ? u2 : u1;
+        float *srw = const_cast<float *>(reinterpret_cast<const float *>(h ? sr2 : sr1));
+        int32_t *ow = const_cast<int32_t *>(h ? o2 : o1);
+        need = min(need, T);
+        while (tp < need) {
+            const int E = min(T - tp, kSortCap);
+            const bool any = tp == 0;
+            const unsigned long long klast =
+                any ? 0ull : ((unsigned long long)__float_as_uint(srw[tp - 1]) << 32) | (uint32_t)ow[tp - 1];
+            unsigned long long prefix = 0, pmask = 0;
+            uint32_t rank = (uint32_t)E;
+            for (int shift = 56; shift >= 0; shift -= 8) {
+                for (int i = threadIdx.x; i < 256; i += NT) S.hist_c[i] = 0;
+                __syncthreads();
+                for (int x = threadIdx.x; x < T; x += NT) {
+                    const unsigned long long key = ((unsigned long long)__float_as_uint(__ldg(u + x)) << 32) | (uint32_t)x;
+                    if ((any || key > klast) && (key & pmask) == prefix)
+                        atomicAdd(&S.hist_c[(key >> shift) & 0xFF], 1u);
+                }
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    uint32_t run = 0;
+                    for (int d = 0; d < 256; d++) {
+                        if (run + S.hist_c[d] >= rank) {
+                            S.tsel_v = d;
+                            S.tsel_below = run;
+                            break;
+                        }
+                        run += S.hist_c[d];
+                    }
+                }
+                __syncthreads();
+                rank -= (uint32_t)S.tsel_below;
+                prefix |= (unsigned long long)S.tsel_v << shift;
+                pmask |= 0xFFull << shift;
+                __syncthreads();
+            }
+            const unsigned long long kE = prefix;  // E-th smallest key after klast
+            if (threadIdx.x == 0) S.tcnt = 0;
+            __syncthreads();
+            for (int x = threadIdx.x; x < T; x += NT) {
+                const unsigned long long key = ((unsigned long long)__float_as_uint(__ldg(u + x)) << 32) | (uint32_t)x;
+                if ((any || key > klast) && key <= kE) S.skey[atomicAdd(&S.tcnt, 1u)] = key;
+            }
+            __syncthreads();
+            int P2 = 1;
+            while (P2 < E) P2 <<= 1;
+            for (int i = E + threadIdx.x; i < P2; i += NT) S.skey[i] = ~0ull;
+            __syncthreads();
+            bitonic_sort_u64(S.skey, P2);
+            for (int i = threadIdx.x; i < E; i += NT) {
+                const unsigned long long kv = S.skey[i];
+                srw[tp + i] = __uint_as_float((uint32_t)(kv >> 32));
+                ow[tp + i] = (int32_t)(kv & 0xFFFFFFFFull);
+            }
+            __syncthreads();
+            tp += E;
+        }
+        if (h) tp2 = tp; else tp1 = tp;
+    }
+
     __device__ __forceinline__ double act_row(int a) const { return a < T ? k1(a) + k2(a) : INFINITY; }
     __device__ __forceinline__ double act_col(int b) const { return b < T - 1 ? k1(b + 1) + k2(b) : INFINITY; }
 
@@ -1037,8 +1107,9 @@ struct Query {
     // is queued for the full-sort retry pass).
     __device__ int run_sparse(int4 *band, int4 *pend, int4 *pend2, int4 *other) {
         const unsigned long long L = (unsigned long long)A.L;
-        const int topP = A.plen ? min(A.plen[qi * 2], A.plen[qi * 2 + 1]) : A.topP;
-        const bool partial = topP < T;
+        tp1 = A.plen ? A.plen[qi * 2] : A.topP;
+        tp2 = A.plen ? A.plen[qi * 2 + 1] : A.topP;
+        const bool partial = tp1 < T || tp2 < T;
         cw = true;
         unsigned long long W = 0;
         int nr = 0, nc = 0, npend = 0;
@@ -1046,7 +1117,11 @@ struct Query {
         for (;;) {
             // the batch probes rows < nr + NB and columns < nc + NB (column b
             // reads position b + 1): stay inside the sorted prefix
-            if (partial && (nr + NB >= topP || nc + NB + 1 >= topP)) return 2;
+            if (partial) {
+                const int need = max(nr + NB, nc + NB + 1) + 1;
+                if (need > tp1) extend(0, need);
+                if (need > tp2) extend(1, need);
+            }
             // next NB lines in activation order (merge path over the two sequences)
             if (threadIdx.x < 32) {
                 const int x = warp_first_false(
@@ -1075,7 +1150,7 @@ struct Query {
                 if (v < nnew) {
                     col = v >= nr2 - nr;
                     idx = col ? nc + (v - (nr2 - nr)) : nr + v;
-                    line = (uint32_t)__ldg((col ? o2 : o1) + idx);
+                    line = (uint32_t)(col ? o2 : o1)[idx];
                     const uint32_t *ptr = col ? A.colptr : A.rowptr;
                     p0 = __ldg(ptr + line);
                     nnz = __ldg(ptr + line + 1) - p0;
@@ -1103,14 +1178,14 @@ struct Query {
                         cj = A.rowcols[t];
                         ci = ln;
                         const float rj = __ldg(u2 + cj), ra = (float)k2(a);
-                        const uint32_t oa = (uint32_t)__ldg(o2 + a);
+                        const uint32_t oa = (uint32_t)o2[a];
                         own = rj > ra || (rj == ra && cj >= oa);
                     } else {  // column position b owns rows of rank > b
                         const int b = -tag - 1;
                         ci = A.colrows[t];
                         cj = ln;
                         const float ri = __ldg(u1 + ci), rb = (float)k1(b);
-                        const uint32_t ob = (uint32_t)__ldg(o1 + b);
+                        const uint32_t ob = (uint32_t)o1[b];
                         own = ri > rb || (ri == rb && ci > ob);
                     }
                     if (!own) continue;
