@@ -154,55 +154,54 @@ def build_workload(cfg, device, rank=0):
 
 # -------------------------------------------------------------------- clocks
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """Samples SM clock and clock-event (throttle) reasons every ~5 ms via NVML
+    while the timed region runs (nvidia-smi's -lms floor is too coarse for a
+    few-hundred-millisecond region)."""
 
-    def __init__(self, index=0):
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
+
+    def __init__(self, index=0, period=0.005):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.period = period
+        self.sm, self.mx, self.flags = [], None, 0
+        self.ok = False
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.th = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.mx = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+            self.stop = threading.Event()
+            self.th = threading.Thread(target=self._run, daemon=True)
             self.th.start()
+            self.ok = True
         except Exception:
-            self.proc = None
+            self.ok = False
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _run(self):
+        nv = self.nv
+        while not self.stop.is_set():
+            try:
+                self.sm.append(float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)))
+                self.flags |= int(nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:
+                pass
+            time.sleep(self.period)
 
     def __exit__(self, *a):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        if self.ok:
+            self.stop.set()
+            self.th.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = max(mx, float(parts[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[3:7]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": float(np.median(self.sm)) if self.sm else None, "sm_max_mhz": self.mx,
+                "reasons": sorted(n for n, b in self.REASONS.items() if self.flags & b),
+                "samples": len(self.sm), "source": "nvml"}
 
 
 # --------------------------------------------------------------- CPU baseline
@@ -244,7 +243,7 @@ def launches_per_step(dix, engine):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c1")
@@ -404,6 +403,12 @@ def main():
     search_ms = float(np.mean(stage_ms[:, 2]))
     alg_bytes = (dix.m + 4) * ncand + 16 * npop
     achieved = alg_bytes / (search_ms / 1e3) / 1e9
+    traffic = None
+    try:  # dram bytes per launch of the same kernel from the committed ncu --set full capture
+        tr = json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())
+        traffic = tr.get(workload, {}).get("dram_bytes_per_launch")
+    except Exception:
+        pass
     line = {
         "metric": metric, "value": value, "unit": "queries/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
@@ -414,7 +419,7 @@ def main():
                      "traverse_scan_topk": search_ms},
         "work_per_step": {"candidates": ncand, "popped_cells": npop, "cand_per_query": ncand / nq},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": HBM_PEAK, "unit": "GB/s",
-                     "frac": achieved / HBM_PEAK, "traffic": None,
+                     "frac": achieved / HBM_PEAK, "traffic": traffic,
                      "kernel": "search_kernel (fused traversal + scan + top-k)",
                      "peak_source": HBM_PEAK_SRC, "alg_bytes_per_launch": alg_bytes},
         "e2e": {"value": e2e_v, "unit": "queries/s", "h2d_bytes_per_step": int(q.numel() * 4),
