@@ -19,17 +19,18 @@ namespace bpq {
 
 namespace {
 
-constexpr int BQ = 128, BT = 128, BK = 8;
+constexpr int BQ = 128, BT = 128, BKC = 32;  // tile 128 x 128, k staged 32 at a time
 
 // dots_h[q, t] = sum_x Q[q, h*dh + x] * C_h[t, x]   (h = blockIdx.z)
-// 128x128 output tile per CTA, 8x8 per thread, k staged 8 at a time.
+// 128x128 output tile per CTA, 8x8 per thread; each k chunk of 32 is loaded
+// with 16-byte loads into k-major shared tiles (one barrier pair per chunk).
 __global__ void __launch_bounds__(256) coarse_dots_kernel(const float *__restrict__ Q, int64_t nq,
                                                           int D, const float *__restrict__ C1,
                                                           const float *__restrict__ C2, int T,
                                                           float *__restrict__ dots1,
                                                           float *__restrict__ dots2) {
-    __shared__ __align__(16) float Qs[BK][BQ];
-    __shared__ __align__(16) float Cs[BK][BT];
+    __shared__ __align__(16) float Qs[BKC][BQ + 4];
+    __shared__ __align__(16) float Cs[BKC][BT + 4];
     const int h = blockIdx.z;
     const int dh = D / 2;
     const float *C = h ? C2 : C1;
@@ -42,21 +43,37 @@ __global__ void __launch_bounds__(256) coarse_dots_kernel(const float *__restric
     for (int i = 0; i < 8; i++)
 #pragma unroll
         for (int j = 0; j < 8; j++) acc[i][j] = 0.f;
-    // loader: 256 threads x 4 = 128 rows x 8 k (per operand)
-    const int lr = threadIdx.x >> 1;        // row 0..127
-    const int lk = (threadIdx.x & 1) * 4;   // k offset 0 or 4
-    for (int k0 = 0; k0 < dh; k0 += BK) {
+    const bool vec = (dh & 3) == 0 && (D & 3) == 0;
+    for (int k0 = 0; k0 < dh; k0 += BKC) {
+        // 128 rows x 32 k per operand = 1024 float4; 256 threads x 4
 #pragma unroll
         for (int u = 0; u < 4; u++) {
-            const int kk = k0 + lk + u;
-            const int64_t q = q0 + lr;
-            const int t = t0 + lr;
-            Qs[lk + u][lr] = (q < nq && kk < dh) ? __ldg(Q + q * D + h * dh + kk) : 0.f;
-            Cs[lk + u][lr] = (t < T && kk < dh) ? __ldg(C + (int64_t)t * dh + kk) : 0.f;
+            const int f = threadIdx.x + u * 256;  // float4 index
+            const int row = f >> 3, kq = (f & 7) * 4;
+            const int kk = k0 + kq;
+            const int64_t q = q0 + row;
+            const int t = t0 + row;
+            float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (vec) {
+                if (q < nq && kk < dh) a = __ldg(reinterpret_cast<const float4 *>(Q + q * D + h * dh + kk));
+                if (t < T && kk < dh) b = __ldg(reinterpret_cast<const float4 *>(C + (int64_t)t * dh + kk));
+            } else {
+                float av[4], bv[4];
+#pragma unroll
+                for (int z = 0; z < 4; z++) {
+                    av[z] = (q < nq && kk + z < dh) ? __ldg(Q + q * D + h * dh + kk + z) : 0.f;
+                    bv[z] = (t < T && kk + z < dh) ? __ldg(C + (int64_t)t * dh + kk + z) : 0.f;
+                }
+                a = make_float4(av[0], av[1], av[2], av[3]);
+                b = make_float4(bv[0], bv[1], bv[2], bv[3]);
+            }
+            Qs[kq + 0][row] = a.x; Qs[kq + 1][row] = a.y; Qs[kq + 2][row] = a.z; Qs[kq + 3][row] = a.w;
+            Cs[kq + 0][row] = b.x; Cs[kq + 1][row] = b.y; Cs[kq + 2][row] = b.z; Cs[kq + 3][row] = b.w;
         }
         __syncthreads();
-#pragma unroll
-        for (int kk = 0; kk < BK; kk++) {
+        const int kn = min(BKC, dh - k0);
+#pragma unroll 8
+        for (int kk = 0; kk < kn; kk++) {
             const float4 a0 = *reinterpret_cast<const float4 *>(&Qs[kk][ty * 4]);
             const float4 a1 = *reinterpret_cast<const float4 *>(&Qs[kk][64 + ty * 4]);
             const float4 b0 = *reinterpret_cast<const float4 *>(&Cs[kk][tx * 4]);
@@ -74,10 +91,17 @@ __global__ void __launch_bounds__(256) coarse_dots_kernel(const float *__restric
     for (int i = 0; i < 8; i++) {
         const int64_t q = q0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
         if (q >= nq) continue;
-#pragma unroll
-        for (int j = 0; j < 8; j++) {
-            const int t = t0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
-            if (t < T) out[q * T + t] = acc[i][j];
+        float *orow = out + q * T;
+        const int tA = t0 + tx * 4, tB = t0 + 64 + tx * 4;
+        if ((T & 3) == 0 && tA + 3 < T) {
+            *reinterpret_cast<float4 *>(orow + tA) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+        } else {
+            for (int j = 0; j < 4; j++) if (tA + j < T) orow[tA + j] = acc[i][j];
+        }
+        if ((T & 3) == 0 && tB + 3 < T) {
+            *reinterpret_cast<float4 *>(orow + tB) = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+        } else {
+            for (int j = 0; j < 4; j++) if (tB + j < T) orow[tB + j] = acc[i][4 + j];
         }
     }
 }
