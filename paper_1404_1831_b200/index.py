@@ -315,6 +315,29 @@ class DeviceIndex:
         _lib.check(rc, "bpq_search")
         return out
 
+    # ------------------------------------------------------------- export
+    def host_arrays(self) -> dict:
+        """The index in the reference's array layout (offsets int64, ids uint32)."""
+        out = dict(c1=self.c1.cpu().numpy(), c2=self.c2.cpu().numpy(),
+                   offsets=self.offsets.cpu().numpy().view(np.uint32).astype(np.int64),
+                   ids=self.ids.cpu().numpy().view(np.uint32), codes=self.codes.cpu().numpy())
+        if self.kind == "hbpq":
+            out.update(bank1=self.bank1.cpu().numpy(), bank2=self.bank2.cpu().numpy())
+        else:
+            out.update(books=self.books.cpu().numpy())
+        return out
+
+    def save(self, index_path, tables_path=None):
+        """Export to BPQI (+ BPQT) in the reference's layout (storage.py:253-343),
+        readable by bilayerpq.load_index / load_tables and its CLI."""
+        from . import storage
+
+        storage.save_index_arrays(index_path, **self.host_arrays())
+        if tables_path is not None and self.kind != "hbpq":
+            storage.save_tables_arrays(tables_path, self.cn1.cpu().numpy(), self.cn2.cpu().numpy(),
+                                       self.fine_norms.cpu().numpy(), self.cross1.cpu().numpy(),
+                                       self.cross2.cpu().numpy())
+
     # --------------------------------------------------------- constructors
     @classmethod
     def from_reference(cls, index, tables=None, device=None):

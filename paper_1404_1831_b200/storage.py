@@ -10,7 +10,10 @@ truncation, trailing bytes), as the reference's strict reader does
 
 from __future__ import annotations
 
+import hashlib
+import os
 import struct
+import tempfile
 from pathlib import Path
 
 import numpy as np
@@ -106,3 +109,86 @@ def load_tables_arrays(path):
            b.arr("<f4", (t, m2, k)))
     b.end()
     return out
+
+
+# --------------------------------------------------------------- write path
+# GPU-built indexes are exported in the reference's own layouts so the
+# reference (storage.load_index / load_tables, CLI) can read them
+# (SURVEY.md §8f row f1).  Field order: storage.py:182-237, 253-281, 332-343.
+
+def _u32(v):
+    return struct.pack("<I", int(v))
+
+
+def _u64(v):
+    return struct.pack("<Q", int(v))
+
+
+def _f32(a):
+    return np.ascontiguousarray(a, "<f4").tobytes()
+
+
+def _atomic_write(path, payload: bytes):
+    path = Path(path)
+    fd, tmp = tempfile.mkstemp(dir=path.parent or Path("."), prefix=path.name + ".")
+    try:
+        with os.fdopen(fd, "wb") as fh:
+            fh.write(payload)
+        os.replace(tmp, path)
+    except BaseException:
+        if os.path.exists(tmp):
+            os.unlink(tmp)
+        raise
+
+
+def index_bytes(c1, c2, offsets, ids, codes, books=None, bank1=None, bank2=None, rotation=None, rot1=None,
+                rot2=None) -> bytes:
+    """BPQI payload for a global-codebook (books) or local-codebook (bank) index."""
+    c1 = np.ascontiguousarray(c1, np.float32)
+    c2 = np.ascontiguousarray(c2, np.float32)
+    codes = np.ascontiguousarray(codes, np.uint8)
+    t, dh = c1.shape
+    d = 2 * dh
+    n, m = codes.shape
+    hb = bank1 is not None
+    k = (np.asarray(bank1).shape[2] if hb else np.asarray(books).shape[1])
+    flags = (FLAG_ROTATED if rotation is not None else 0) | (FLAG_HBPQ if hb else 0)
+    out = [b"BPQI", _u32(FORMAT_VERSION), _u32(d), _u32(t), _u32(m), _u32(k), _u32(flags), _u64(n)]
+    out += [_u32(t), _u32(dh), _u32(1 if rotation is not None else 0), _f32(c1), _f32(c2)]
+    if rotation is not None:
+        out.append(_f32(rotation))
+    out += [np.ascontiguousarray(offsets, "<i8").tobytes(), np.ascontiguousarray(ids, "<u4").tobytes(),
+            codes.tobytes()]
+    if hb:
+        b1 = np.ascontiguousarray(bank1, np.float32)
+        bt, m2, bk, ds = b1.shape
+        out += [_u32(bt), _u32(m2), _u32(bk), _u32(ds), _u32(1 if rot1 is not None else 0),
+                _u32(1 if rot2 is not None else 0), _f32(b1), _f32(bank2)]
+        if rot1 is not None:
+            out.append(_f32(rot1))
+        if rot2 is not None:
+            out.append(_f32(rot2))
+    else:
+        out.append(_f32(books))
+    return b"".join(out)
+
+
+def tables_bytes(cn1, cn2, fine_norms, cross1, cross2) -> bytes:
+    """BPQT payload (query-independent FBPQ tables)."""
+    t = np.asarray(cn1).shape[0]
+    m, k = np.asarray(fine_norms).shape
+    return b"".join([b"BPQT", _u32(FORMAT_VERSION), _u32(t), _u32(m), _u32(k), _f32(cn1), _f32(cn2),
+                     _f32(fine_norms), _f32(cross1), _f32(cross2)])
+
+
+def save_index_arrays(path, **arrays) -> str:
+    """Write a BPQI file atomically; returns its sha256."""
+    payload = index_bytes(**arrays)
+    _atomic_write(path, payload)
+    return hashlib.sha256(payload).hexdigest()
+
+
+def save_tables_arrays(path, cn1, cn2, fine_norms, cross1, cross2) -> str:
+    payload = tables_bytes(cn1, cn2, fine_norms, cross1, cross2)
+    _atomic_write(path, payload)
+    return hashlib.sha256(payload).hexdigest()

@@ -244,8 +244,37 @@ def make_hbpq():
     print(f"hbpq done in {time.time() - t0:.1f}s")
 
 
+def make_storage():
+    """sha256 of the reference's own BPQI/BPQT bytes for the c0 and HBPQ rigs."""
+    import hashlib
+    import json
+
+    from bilayerpq import storage as rst
+    from bilayerpq.hbpq import HbpqIndex, LocalCodebookBank
+    from bilayerpq.fbpq import FbpqTables
+
+    g = np.load(OUT / "c0.npz")
+    idx = bq.MultiIndex(bq.CoarsePair(bq.Codebook(g["c1"]), bq.Codebook(g["c2"])), bq.CellTable(g["offsets"]),
+                        g["ids"], g["codes"], bq.PqCodec(g["books"]))
+    tabs = FbpqTables(g["cn1"], g["cn2"], g["fine_norms"], g["cross1"], g["cross2"])
+    h = np.load(OUT / "hbpq.npz")
+    hidx = HbpqIndex(bq.CoarsePair(bq.Codebook(h["c1"]), bq.Codebook(h["c2"])), bq.CellTable(h["offsets"]),
+                     h["ids"], h["hcodes"], LocalCodebookBank(h["bank1"], h["bank2"]))
+    import tempfile, os
+    with tempfile.TemporaryDirectory() as d:
+        rst.save_tables(tabs, os.path.join(d, "t.bpqt"))
+        tb = open(os.path.join(d, "t.bpqt"), "rb").read()
+    out = {"c0_bpqi_sha256": hashlib.sha256(rst.index_to_bytes(idx)).hexdigest(),
+           "c0_bpqt_sha256": hashlib.sha256(tb).hexdigest(),
+           "hbpq_bpqi_sha256": hashlib.sha256(rst.index_to_bytes(hidx)).hexdigest()}
+    (OUT / "storage_sha256.json").write_text(json.dumps(out, indent=1))
+    print("storage:", out)
+
+
 if __name__ == "__main__":
-    what = sys.argv[1:] or ["kat", "c0", "hbpq"]
+    what = sys.argv[1:] or ["kat", "c0", "hbpq", "storage"]
+    if "storage" in what:
+        make_storage()
     if "kat" in what:
         make_kat()
     if "c0" in what:

@@ -345,3 +345,21 @@ def test_scale_sparse_index_vs_oracle(torch_cuda, oracle):
         assert (res.ncand.cpu().numpy() >= min(L, 1_000_000)).all()
         wd, wi, wc, wn = oracle.search_batch_c(idx, "fbpq", q[:48], L, k, threads=8)
         check_topk(d[:48], i_[:48], c[:48], wd, wi, wc, _qn(q[:48]), min_exact_frac=0.9)
+
+
+def test_export_round_trip_through_bpqi(c0, c0_index, tmp_path):
+    """A device index exported to BPQI/BPQT (reference layout) and reloaded
+    searches identically."""
+    import hashlib
+    import json
+    from pathlib import Path
+
+    from paper_1404_1831_b200 import DeviceIndex
+
+    c0_index.save(tmp_path / "i.bpqi", tmp_path / "t.bpqt")
+    sha = json.loads((Path(__file__).resolve().parent / "golden" / "storage_sha256.json").read_text())
+    assert hashlib.sha256((tmp_path / "i.bpqi").read_bytes()).hexdigest() == sha["c0_bpqi_sha256"]
+    back = DeviceIndex.load(tmp_path / "i.bpqi", tmp_path / "t.bpqt")
+    q = c0["queries"][:50].astype(np.float32)
+    for x, y in zip(c0_index.search(q, 5000, 50).numpy(), back.search(q, 5000, 50).numpy()):
+        np.testing.assert_array_equal(x, y)
