@@ -78,6 +78,11 @@ typedef struct bpq_index_desc {
      * line holds fewer populated cells than the segment has cells. */
     const uint32_t *row_ptr, *col_ptr;   /* [T+1] */
     const uint16_t *row_cols, *col_rows; /* [min(N_global, T*T)] capacity */
+    /* Optional OPQ rotations (the paper's "optimized" variants): the coarse
+     * pair's R [D, D] applied to queries as q @ R (multi_index.py:67-74), and
+     * the bank's per-half R1, R2 [D/2, D/2] applied to the query
+     * displacements of HBPQ (hbpq.py:328-331).  NULL = none. */
+    const float *rotation, *rot1, *rot2;
 } bpq_index_desc;
 
 typedef struct bpq_index bpq_index;
@@ -179,6 +184,9 @@ int bpq_build_cell_lists(const uint32_t *offsets, int32_t t, uint32_t *row_ptr, 
  * idle) when the library was built with -DBPQ_PHASE_PROF; returns 1 if
  * compiled in, else 0 (and the buffer is never written). */
 int bpq_debug_set_phase_buffer(unsigned long long *dev_counters);
+
+/* out[n, d] = x[n, d] @ R[d, d] (row-vector rotation, quantizer.py:95-96). */
+int bpq_rotate(const float *x, int64_t n, int32_t d, const float *R, float *out, void *stream);
 
 /* Merge per-shard top-k lists [g, nq, k] into [nq, k] by (dist, id). */
 int bpq_merge_topk(const float *dists, const uint32_t *ids, const int32_t *counts, int32_t g,

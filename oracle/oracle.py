@@ -171,11 +171,15 @@ def coarse_norms(c):
     return np.einsum("ij,ij->i", c, c)
 
 
-def coarse_scan(c1, c2, q):
-    """bpq/multi_index.py:270-293 (no rotation): (qr, dots1, dots2, r1, r2)."""
+def coarse_scan(c1, c2, q, rotation=None):
+    """bpq/multi_index.py:270-293: (qr, dots1, dots2, r1, r2); qr = q @ R
+    when the pair carries a rotation (multi_index.py:67-74, quantizer.py:95-96)."""
     c1 = _c(c1, np.float32)
     c2 = _c(c2, np.float32)
-    qr = np.asarray(q, np.float32).reshape(-1)
+    qr = np.asarray(q, np.float32).reshape(1, -1)
+    if rotation is not None:
+        qr = qr @ _c(rotation, np.float32)
+    qr = qr[0]
     dh = c1.shape[1]
     q1 = qr[:dh]
     q2 = qr[dh:]
@@ -228,9 +232,9 @@ def build_tables_from(c1, c2, books):
     return cn1, cn2, fine_norms, cross1, cross2
 
 
-def prepare_query(c1, c2, books, fine_norms, q):
+def prepare_query(c1, c2, books, fine_norms, q, rotation=None):
     """bpq/fbpq.py:129-145 -> (q_norm, dots1, dots2, fold, r1, r2)."""
-    qr, dots1, dots2, r1, r2 = coarse_scan(c1, c2, q)
+    qr, dots1, dots2, r1, r2 = coarse_scan(c1, c2, q, rotation)
     books = _c(books, np.float32)
     m, k, ds = books.shape
     qdot_fine = np.empty((m, k), np.float32)
@@ -245,7 +249,11 @@ class Index:
     """Plain arrays of a built multi-index (bpq/multi_index.py:100-146 /
     bpq/hbpq.py:240-290), optionally with FBPQ tables (bpq/fbpq.py:28-66)."""
 
-    def __init__(self, c1, c2, offsets, ids, codes, books=None, bank1=None, bank2=None, tables=None):
+    def __init__(self, c1, c2, offsets, ids, codes, books=None, bank1=None, bank2=None, tables=None,
+                 rotation=None, rot1=None, rot2=None):
+        self.rotation = None if rotation is None else _c(rotation, np.float32)
+        self.rot1 = None if rot1 is None else _c(rot1, np.float32)
+        self.rot2 = None if rot2 is None else _c(rot2, np.float32)
         self.c1 = _c(c1, np.float32)
         self.c2 = _c(c2, np.float32)
         self.offsets = _c(offsets, np.int64)
@@ -272,14 +280,19 @@ def scan_query(index: Index, engine: str, q, l):
     scan_hbpq (hbpq.py:316-334, no rotations)."""
     if engine == "fbpq":
         cn1, cn2, fine_norms, cross1, cross2 = index.tables
-        q_norm, d1, d2, fold, r1, r2 = prepare_query(index.c1, index.c2, index.books, fine_norms, q)
+        q_norm, d1, d2, fold, r1, r2 = prepare_query(index.c1, index.c2, index.books, fine_norms, q, index.rotation)
         vis = traverse(index.offsets, r1, r2, l)
         return scan_tables(*vis, index.ids, index.codes, q_norm, d1, d2, cn1, cn2, fold, cross1, cross2)
-    qr, _, _, r1, r2 = coarse_scan(index.c1, index.c2, q)
+    qr, _, _, r1, r2 = coarse_scan(index.c1, index.c2, q, index.rotation)
     vis = traverse(index.offsets, r1, r2, l)
     dh = index.c1.shape[1]
     e1 = qr[None, :dh] - index.c1
     e2 = qr[None, dh:] - index.c2
+    if engine == "hbpq":  # per-half bank rotations (hbpq.py:328-331)
+        if index.rot1 is not None:
+            e1 = np.asarray(e1, np.float32) @ index.rot1
+        if index.rot2 is not None:
+            e2 = np.asarray(e2, np.float32) @ index.rot2
     if engine == "baseline":
         return scan_global(*vis, index.ids, index.codes, e1, e2, index.books)
     if engine == "hbpq":

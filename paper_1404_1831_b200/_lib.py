@@ -51,6 +51,9 @@ class IndexDesc(ctypes.Structure):
         ("col_ptr", P),
         ("row_cols", P),
         ("col_rows", P),
+        ("rotation", P),
+        ("rot1", P),
+        ("rot2", P),
     ]
 
 
@@ -76,6 +79,7 @@ SIGNATURES = {
     "bpq_cell_lists_workspace_size": (SZ, [I32]),
     "bpq_build_cell_lists": (ctypes.c_int, [P, I32, P, P, P, P, P, SZ, P]),
     "bpq_debug_set_phase_buffer": (ctypes.c_int, [P]),
+    "bpq_rotate": (ctypes.c_int, [P, I64, I32, P, P, P]),
     "bpq_merge_topk": (ctypes.c_int, [P, P, P, I32, I64, I32, P, P, P, P]),
 }
 

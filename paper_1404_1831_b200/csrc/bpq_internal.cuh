@@ -50,6 +50,7 @@ struct Index {
     const uint32_t *ids;
     const uint8_t *codes;
     const float *books, *fine_norms, *cross1, *cross2, *bank1, *bank2;
+    const float *rot, *rot1, *rot2;  // optional rotations (see bpq_index_desc)
     // populated-cell lists (optional): row i -> columns j, column j -> rows i
     const uint32_t *rowptr, *colptr;
     const uint16_t *rowcols, *colrows;
@@ -73,7 +74,7 @@ int launch_row_topk(const float *queries, int64_t nq, int32_t D, const float *do
                     cudaStream_t stream);
 
 struct SearchWorkspace {
-    float *dots1, *dots2, *sr1, *sr2, *fold, *ru1, *ru2;
+    float *dots1, *dots2, *sr1, *sr2, *fold, *ru1, *ru2, *qrot;
     int32_t *ord1, *ord2, *pos1, *pos2;
     unsigned int *retry_list, *retry_count;
     int topP;                      // sorted prefix length in sr/ord for this launch (full: T)
@@ -85,7 +86,8 @@ struct SearchWorkspace {
     int n_cta;
 };
 
-size_t search_cta_scratch_bytes(int32_t T);
+size_t search_cta_scratch_bytes(int32_t T, int32_t D);
+int launch_rotate(const float *x, int64_t n, int32_t d, const float *R, float *out, cudaStream_t stream);
 int search_grid_ctas(int engine, int M);
 int launch_search(const Index &ix, int engine, const float *queries, int64_t q0, int64_t nq,
                   int64_t budget, int32_t k, const SearchWorkspace &ws, float *out_dist,

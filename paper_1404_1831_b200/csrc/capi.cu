@@ -23,7 +23,7 @@ size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct SearchLayout {
     int64_t chunk;
-    size_t dots1, dots2, sr1, sr2, ord1, ord2, pos1, pos2, fold, ru1, ru2, retry, plen, counter, cta, cta_stride, total;
+    size_t dots1, dots2, sr1, sr2, ord1, ord2, pos1, pos2, fold, ru1, ru2, retry, plen, qrot, counter, cta, cta_stride, total;
     int n_cta;
 };
 
@@ -56,8 +56,9 @@ bool layout_for(const Index &ix, int64_t nq, SearchLayout *L) {
     s.ru2 = o; o += al(row);
     s.retry = o; o += al((size_t)s.chunk * 4 + 4);
     s.plen = o; o += al((size_t)s.chunk * 8);
+    s.qrot = o; o += ix.rot ? al((size_t)s.chunk * ix.D * 4) : 0;
     s.counter = o; o += al(4);
-    s.cta_stride = al(search_cta_scratch_bytes(ix.T));
+    s.cta_stride = al(search_cta_scratch_bytes(ix.T, ix.D));
     s.cta = o; o += s.cta_stride * n_cta;
     s.total = o;
     *L = s;
@@ -143,6 +144,9 @@ extern "C" int bpq_index_create(const bpq_index_desc *d, int copy_from_host, bpq
         ix.rowcols = d->row_cols;
         ix.colptr = d->col_ptr;
         ix.colrows = d->col_rows;
+        ix.rot = d->rotation;
+        ix.rot1 = d->rot1;
+        ix.rot2 = d->rot2;
     } else {
         int rc = 0;
         rc |= copy_in(d->coarse1, T * dh, ix.owned, &ix.c1);
@@ -162,7 +166,9 @@ extern "C" int bpq_index_create(const bpq_index_desc *d, int copy_from_host, bpq
         rc |= copy_in(d->cross2, T * (M / 2) * K, ix.owned, &ix.cross2);
         rc |= copy_in(d->bank1, T * (M / 2) * K * ds, ix.owned, &ix.bank1);
         rc |= copy_in(d->bank2, T * (M / 2) * K * ds, ix.owned, &ix.bank2);
-        (void)D;
+        rc |= copy_in(d->rotation, D * D, ix.owned, &ix.rot);
+        rc |= copy_in(d->rot1, dh * dh, ix.owned, &ix.rot1);
+        rc |= copy_in(d->rot2, dh * dh, ix.owned, &ix.rot2);
         ix.rowptr = ix.colptr = nullptr;
         ix.rowcols = ix.colrows = nullptr;
         if (d->row_ptr && d->col_ptr && d->row_cols && d->col_rows) {
@@ -256,6 +262,7 @@ extern "C" int bpq_search_ex(const bpq_index *index, int engine, const float *qu
     ws.retry_count = reinterpret_cast<unsigned int *>(w + L.retry);
     ws.retry_list = ws.retry_count + 1;
     ws.plen = reinterpret_cast<int32_t *>(w + L.plen);
+    ws.qrot = ix.rot ? reinterpret_cast<float *>(w + L.qrot) : nullptr;
     ws.qlist = nullptr;
     ws.qlist_count = nullptr;
     ws.counter = reinterpret_cast<unsigned int *>(w + L.counter);
@@ -268,6 +275,11 @@ extern "C" int bpq_search_ex(const bpq_index *index, int engine, const float *qu
     for (int64_t q0 = 0; q0 < nq; q0 += L.chunk) {
         int64_t n = std::min<int64_t>(L.chunk, nq - q0);
         const float *qc = queries + q0 * ix.D;
+        if (ix.rot) {  // queries into the index's rotated space (CoarsePair.rotate_in)
+            int rr = launch_rotate(qc, n, ix.D, ix.rot, ws.qrot, s);
+            if (rr) return rr;
+            qc = ws.qrot;
+        }
         int rc = launch_coarse_dots(qc, n, ix.D, ix.c1, ix.c2, ix.T, ws.dots1, ws.dots2, s);
         if (rc) return rc;
         if (ev) BPQ_CUDA_TRY(cudaEventRecord((cudaEvent_t)stage_events[1], s));

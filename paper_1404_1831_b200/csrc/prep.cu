@@ -511,4 +511,56 @@ int launch_row_topk(const float *queries, int64_t nq, int32_t D, const float *do
     return fail(BPQ_ERR_UNSUPPORTED, "num_coarse > 16384 is outside the row-sort kernel range");
 }
 
+namespace {
+// out[q][x] = sum_y X[q][y] * R[y][x]: 64x64 tiles, 4x4 per thread (FFMA).
+__global__ void __launch_bounds__(256) rotate_kernel(const float *__restrict__ X, int64_t n, int d,
+                                                     const float *__restrict__ R, float *__restrict__ out) {
+    __shared__ float Xs[16][64 + 4];
+    __shared__ float Rs[16][64 + 4];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int64_t q0 = (int64_t)blockIdx.y * 64;
+    const int x0 = blockIdx.x * 64;
+    float acc[4][4] = {};
+    for (int k0 = 0; k0 < d; k0 += 16) {
+        for (int f = threadIdx.x; f < 64 * 16; f += 256) {
+            const int r = f >> 4, kk = f & 15;      // X tile: row r, k kk
+            const int64_t q = q0 + r;
+            Xs[kk][r] = (q < n && k0 + kk < d) ? __ldg(X + q * d + k0 + kk) : 0.f;
+            const int kr = f >> 6, c = f & 63;      // R tile: k kr, column c
+            Rs[kr][c] = (k0 + kr < d && x0 + c < d) ? __ldg(R + (int64_t)(k0 + kr) * d + x0 + c) : 0.f;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < 16; kk++) {
+#pragma unroll
+            for (int i = 0; i < 4; i++)
+#pragma unroll
+                for (int j = 0; j < 4; j++) acc[i][j] = fmaf(Xs[kk][ty * 4 + i], Rs[kk][tx * 4 + j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+    for (int i = 0; i < 4; i++) {
+        const int64_t q = q0 + ty * 4 + i;
+        if (q >= n) continue;
+        for (int j = 0; j < 4; j++) {
+            const int x = x0 + tx * 4 + j;
+            if (x < d) out[q * d + x] = acc[i][j];
+        }
+    }
+}
+}  // namespace
+
+int launch_rotate(const float *x, int64_t n, int32_t d, const float *R, float *out, cudaStream_t stream) {
+    if (n == 0) return BPQ_OK;
+    dim3 grid((d + 63) / 64, (unsigned)((n + 63) / 64));
+    rotate_kernel<<<grid, 256, 0, stream>>>(x, n, d, R, out);
+    BPQ_CUDA_TRY(cudaGetLastError());
+    return BPQ_OK;
+}
+
 }  // namespace bpq
+
+extern "C" int bpq_rotate(const float *x, int64_t n, int32_t d, const float *R, float *out, void *stream) {
+    BPQ_CHECK(n >= 0 && d >= 1 && x && R && out, BPQ_ERR_INVALID, "bad rotate arguments");
+    return bpq::launch_rotate(x, n, d, R, out, (cudaStream_t)stream);
+}

@@ -136,7 +136,7 @@ TravLayout trav_layout(int64_t t, int64_t budget, int64_t total) {
     L.cap = cap;
     size_t o = 0;
     L.off_scratch = o;
-    o += al(search_cta_scratch_bytes((int32_t)t));
+    o += al(search_cta_scratch_bytes((int32_t)t, 0));
     L.off_key = o; o += al(cap * 8);
     L.off_lin = o; o += al(cap * 4);
     L.off_st = o; o += al(cap * 8);
@@ -159,9 +159,10 @@ TravLayout trav_layout(int64_t t, int64_t budget, int64_t total) {
 
 }  // namespace
 
-size_t search_cta_scratch_bytes(int32_t T) {
+size_t search_cta_scratch_bytes(int32_t T, int32_t D) {
+    // row/column state, segments, four cell lists, rotated query displacements (HBPQ)
     return (((size_t)6 * T * 4 + 15) & ~(size_t)15) + (size_t)2 * T * sizeof(uint4) +
-           (size_t)4 * kBandCap * sizeof(int4);
+           (size_t)4 * kBandCap * sizeof(int4) + (size_t)kSearchThreads * D * 4;
 }
 
 

@@ -127,6 +127,7 @@ struct Args {
     const uint32_t *ids;
     const uint8_t *codes;
     const float *books, *fine_norms, *cross1, *cross2, *bank1, *bank2;
+    const float *rot1, *rot2;  // HBPQ per-half rotations (optional)
     double rho;
     unsigned long long n_global;
     const float *queries;
@@ -319,7 +320,7 @@ __device__ __forceinline__ float dist_fbpq(const Args<KT, OffT> &A, const float 
 // d = e - book, acc += d*d sequentially (numba_backend.py:165-176, 198-210).
 template <int ENGINE, int MT, typename KT, typename OffT>
 __device__ __forceinline__ float dist_recon(const Args<KT, OffT> &A, const float *tab, int oi, int oj,
-                                            const uint32_t (&w)[4]) {
+                                            const uint32_t (&w)[4], const float *erow = nullptr) {
     const int M = MT ? MT : A.M;
     const int M2 = M / 2;
     const int K = A.K, ds = A.ds, dh = A.dh;
@@ -336,7 +337,13 @@ __device__ __forceinline__ float dist_recon(const Args<KT, OffT> &A, const float
             bk = (p < M2 ? A.bank1 : A.bank2) + (((size_t)row * M2 + hp) * K + c) * ds;
         else
             bk = A.books + ((size_t)p * K + c) * ds;
-        if ((ds & 3) == 0) {
+        if (erow != nullptr) {  // rotated displacement row (HBPQ with bank rotations)
+            const float *er = erow + (p < M2 ? 0 : dh) + hp * ds;
+            for (int u = 0; u < ds; u++) {
+                float d = __fsub_rn(er[u], __ldg(bk + u));
+                acc = __fadd_rn(acc, __fmul_rn(d, d));
+            }
+        } else if ((ds & 3) == 0) {
             for (int u = 0; u < ds; u += 4) {
                 const float4 cv = __ldg(reinterpret_cast<const float4 *>(cr + u));
                 const float4 bv = __ldg(reinterpret_cast<const float4 *>(bk + u));
@@ -463,6 +470,7 @@ struct Query {
     const int32_t *p1, *p2;  // codeword -> sorted position
     const float *d1, *d2;
     const float *u1, *u2;    // unsorted half-distances (codeword-keyed entries)
+    float *erot;             // [NT][D] rotated displacement rows of the current chunk (HBPQ)
     bool cw;                 // list entries hold codewords (i, j) instead of positions (a, b)
     int T, P, M;
     int tp1, tp2;              // valid sorted prefix per half (partial sort), block-uniform
@@ -486,6 +494,7 @@ struct Query {
         u1 = A.ru1 ? A.ru1 + q * T : nullptr;
         u2 = A.ru2 ? A.ru2 + q * T : nullptr;
         cw = false;
+        erot = nullptr;
         ncand = 0;
         popped = 0;
     }
@@ -646,6 +655,28 @@ struct Query {
                 S.cbase[threadIdx.x] = cb;
                 S.ccnt[threadIdx.x] = lc;
                 if (big) S.bigs[atomicAdd(&S.nbig, 1u)] = (uint16_t)threadIdx.x;
+                if constexpr (ENGINE == BPQ_ENGINE_HBPQ) {
+                    if (erot != nullptr && lc > 0) {
+                        // e_h = (q_h - c_h[row]) @ R_h per half (hbpq.py:326-331)
+                        const int dh = A.dh;
+                        float *er = erot + (size_t)threadIdx.x * A.D;
+                        for (int h = 0; h < 2; h++) {
+                            const float *R = h ? A.rot2 : A.rot1;
+                            const float *cr = (h ? A.c2 : A.c1) + (size_t)(h ? oj : oi) * dh;
+                            const float *qh = tab + h * dh;
+                            for (int x = 0; x < dh; x++) {
+                                if (R == nullptr) {
+                                    er[h * dh + x] = __fsub_rn(qh[x], __ldg(cr + x));
+                                } else {
+                                    float acc = 0.f;
+                                    for (int y = 0; y < dh; y++)
+                                        acc = fmaf(__fsub_rn(qh[y], __ldg(cr + y)), __ldg(R + (size_t)y * dh + x), acc);
+                                    er[h * dh + x] = acc;
+                                }
+                            }
+                        }
+                    }
+                }
                 __syncthreads();
                 ncand += E;
                 for (uint32_t e0 = 0; e0 < E; e0 += NT * kUnroll) {
@@ -675,7 +706,8 @@ struct Query {
                         if constexpr (ENGINE == BPQ_ENGINE_FBPQ)
                             dist = dist_fbpq<MT>(A, tab, S.coi[lo], S.coj[lo], S.cbase[lo], w[u]);
                         else
-                            dist = dist_recon<ENGINE, MT>(A, tab, S.coi[lo], S.coj[lo], w[u]);
+                            dist = dist_recon<ENGINE, MT>(A, tab, S.coi[lo], S.coj[lo], w[u],
+                                                          erot ? erot + (size_t)lo * A.D : nullptr);
                         offer_lazy(dist, A.ids + entry[u]);
                     }
                     round_end();
@@ -1267,6 +1299,8 @@ struct Query {
         int4 *listB = listA + kBandCap;
         int4 *listC = listB + kBandCap;
         int4 *listD = listC + kBandCap;
+        if constexpr (ENGINE == BPQ_ENGINE_HBPQ)
+            erot = (A.rot1 != nullptr || A.rot2 != nullptr) ? reinterpret_cast<float *>(listD + kBandCap) : nullptr;
 
         if (threadIdx.x == 0) {
             S.ntk = 0;
@@ -1697,6 +1731,8 @@ int launch_one(const Index &ix, const float *queries, int64_t q0, int64_t nq, in
     A.cross2 = ix.cross2;
     A.bank1 = ix.bank1;
     A.bank2 = ix.bank2;
+    A.rot1 = ix.rot1;
+    A.rot2 = ix.rot2;
     A.n_global = (unsigned long long)ix.N_global;
     A.rho = (double)(ix.N_global > 0 ? ix.N_global : 1) / ((double)ix.T * ix.T);
     A.queries = queries;

@@ -125,13 +125,29 @@ def pack_cells(i_idx, j_idx, codes, t, id_offset=0, *, stream=None):
     return offsets, ids, out_codes
 
 
-def build_index(base, c1, c2, books, id_offset=0, *, tables=None, device=None):
+def rotate(xs, R, *, stream=None):
+    """xs @ R on the device (Rotation.rotate, quantizer.py:95-96)."""
+    import torch
+
+    xs = _t(xs, xs.device if isinstance(xs, torch.Tensor) else "cuda", torch.float32)
+    Rt = _t(R, xs.device, torch.float32)
+    out = torch.empty_like(xs)
+    lib = _lib.load()
+    _lib.check(lib.bpq_rotate(_lib.ptr(xs), xs.shape[0], xs.shape[1], _lib.ptr(Rt), _lib.ptr(out),
+                              _lib.stream_ptr(stream)), "rotate")
+    return out
+
+
+def build_index(base, c1, c2, books, id_offset=0, *, tables=None, device=None, rotation=None):
     """Assign, encode and pack ``base`` into a DeviceIndex (build_index,
-    multi_index.py:210-230)."""
+    multi_index.py:210-230); with a coarse rotation the vectors are encoded
+    in the rotated space (displacements, multi_index.py:181-189)."""
     import torch
 
     dev = torch.device(device or "cuda")
     xs = _t(base, dev, torch.float32)
+    if rotation is not None:
+        xs = rotate(xs, rotation)
     c1n = c1.cpu().numpy() if isinstance(c1, torch.Tensor) else np.asarray(c1, np.float32)
     c2n = c2.cpu().numpy() if isinstance(c2, torch.Tensor) else np.asarray(c2, np.float32)
     booksn = books.cpu().numpy() if isinstance(books, torch.Tensor) else np.asarray(books, np.float32)
@@ -143,7 +159,7 @@ def build_index(base, c1, c2, books, id_offset=0, *, tables=None, device=None):
     if tables is None:
         tables = build_tables_host(c1n, c2n, booksn)
     return DeviceIndex(c1=c1n, c2=c2n, offsets=offsets, ids=ids, codes=pcodes, books=booksn,
-                       tables=tables, device=dev)
+                       tables=tables, device=dev, rotation=rotation)
 
 
 def build_index_streamed(n, make_chunk, c1, c2, books, id_offset=0, *, chunk=1 << 24, tables=None, device=None):
@@ -180,19 +196,34 @@ def build_index_streamed(n, make_chunk, c1, c2, books, id_offset=0, *, chunk=1 <
                        tables=tables, device=dev)
 
 
-def build_hbpq_index(base, c1, c2, bank1, bank2, id_offset=0, *, device=None):
-    """build_hbpq_index (hbpq.py:293-313) on the device."""
+def build_hbpq_index(base, c1, c2, bank1, bank2, id_offset=0, *, device=None, rotation=None, rot1=None,
+                     rot2=None):
+    """build_hbpq_index (hbpq.py:293-313) on the device, with the optional
+    coarse rotation and per-half bank rotations (hbpq.py:168-187)."""
     import torch
 
     dev = torch.device(device or "cuda")
     xs = _t(base, dev, torch.float32)
+    if rotation is not None:
+        xs = rotate(xs, rotation)
     c1n, c2n = np.asarray(c1, np.float32), np.asarray(c2, np.float32)
-    t = c1n.shape[0]
+    t, dh = c1n.shape
     i_idx, j_idx = assign_cells(xs, c1n, c2n)
-    codes = encode_local(xs, i_idx, j_idx, c1n, c2n, bank1, bank2)
+    if rot1 is None and rot2 is None:
+        codes = encode_local(xs, i_idx, j_idx, c1n, c2n, bank1, bank2)
+    else:
+        # rotated half displacements, encoded against zero "coarse" books
+        disp = xs - torch.cat([torch.from_numpy(c1n).to(dev)[i_idx], torch.from_numpy(c2n).to(dev)[j_idx]], 1)
+        h1, h2 = disp[:, :dh].contiguous(), disp[:, dh:].contiguous()
+        if rot1 is not None:
+            h1 = rotate(h1, rot1)
+        if rot2 is not None:
+            h2 = rotate(h2, rot2)
+        zeros = np.zeros_like(c1n)
+        codes = encode_local(torch.cat([h1, h2], 1).contiguous(), i_idx, j_idx, zeros, zeros, bank1, bank2)
     offsets, ids, pcodes = pack_cells(i_idx, j_idx, codes, t, id_offset)
     return DeviceIndex(c1=c1n, c2=c2n, offsets=offsets, ids=ids, codes=pcodes, bank1=bank1,
-                       bank2=bank2, device=dev)
+                       bank2=bank2, device=dev, rotation=rotation, rot1=rot1, rot2=rot2)
 
 
 def train_kmeans(xs, k, iters=10, seed=0):

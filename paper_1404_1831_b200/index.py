@@ -105,7 +105,8 @@ class DeviceIndex:
     streams as long as each uses its own workspace (``workspace=``)."""
 
     def __init__(self, *, c1, c2, offsets, ids, codes, books=None, tables=None, bank1=None,
-                 bank2=None, global_offsets=None, device=None, num_entries_global=None, cell_lists="auto"):
+                 bank2=None, global_offsets=None, device=None, num_entries_global=None, cell_lists="auto",
+                 rotation=None, rot1=None, rot2=None):
         import torch
 
         self.device = torch.device(device if device is not None else "cuda")
@@ -170,6 +171,15 @@ class DeviceIndex:
             self.cross2 = _f32(_table_attr(tables, 4), dev)
         self.bank1 = _f32(bank1, dev)
         self.bank2 = _f32(bank2, dev)
+        # OPQ rotations: coarse pair R [D, D] (queries -> q @ R), bank R1/R2 [D/2, D/2]
+        self.rotation = _f32(rotation, dev)
+        self.rot1 = _f32(rot1, dev) if self.kind == "hbpq" else None
+        self.rot2 = _f32(rot2, dev) if self.kind == "hbpq" else None
+        if self.rotation is not None and tuple(self.rotation.shape) != (self.dim, self.dim):
+            raise ValueError("rotation dimension does not match the codebooks")
+        for r in (self.rot1, self.rot2):
+            if r is not None and tuple(r.shape) != (self.dim // 2, self.dim // 2):
+                raise ValueError("per-half rotation dimension must equal dim/2")
         self._build_cell_lists(cell_lists)
         self._handle = None
         self._ws = None
@@ -220,6 +230,7 @@ class DeviceIndex:
         d.bank1, d.bank2 = _lib.ptr(self.bank1), _lib.ptr(self.bank2)
         d.row_ptr, d.col_ptr = _lib.ptr(self.row_ptr), _lib.ptr(self.col_ptr)
         d.row_cols, d.col_rows = _lib.ptr(self.row_cols), _lib.ptr(self.col_rows)
+        d.rotation, d.rot1, d.rot2 = _lib.ptr(self.rotation), _lib.ptr(self.rot1), _lib.ptr(self.rot2)
         h = ctypes.c_void_p()
         _lib.check(lib.bpq_index_create(ctypes.byref(d), 0, ctypes.byref(h)), "bpq_index_create")
         self._handle = h
@@ -321,8 +332,12 @@ class DeviceIndex:
         out = dict(c1=self.c1.cpu().numpy(), c2=self.c2.cpu().numpy(),
                    offsets=self.offsets.cpu().numpy().view(np.uint32).astype(np.int64),
                    ids=self.ids.cpu().numpy().view(np.uint32), codes=self.codes.cpu().numpy())
+        if self.rotation is not None:
+            out["rotation"] = self.rotation.cpu().numpy()
         if self.kind == "hbpq":
-            out.update(bank1=self.bank1.cpu().numpy(), bank2=self.bank2.cpu().numpy())
+            out.update(bank1=self.bank1.cpu().numpy(), bank2=self.bank2.cpu().numpy(),
+                       rot1=None if self.rot1 is None else self.rot1.cpu().numpy(),
+                       rot2=None if self.rot2 is None else self.rot2.cpu().numpy())
         else:
             out.update(books=self.books.cpu().numpy())
         return out
@@ -345,16 +360,16 @@ class DeviceIndex:
         object with .coarse.book1.centroids, .cells.offsets, .ids, .codes and
         .fine.codebooks or .bank.books1/.books2), plus optional FbpqTables."""
         coarse = index.coarse
-        if getattr(coarse, "rotation", None) is not None:
-            raise NotImplementedError("OPQ-rotated coarse pairs are not supported yet (SURVEY §8f f3)")
+        rot = getattr(coarse, "rotation", None)
         c1 = coarse.book1.centroids
         c2 = coarse.book2.centroids
         bank = getattr(index, "bank", None)
-        kw = dict(c1=c1, c2=c2, offsets=index.cells.offsets, ids=index.ids, codes=index.codes, device=device)
+        kw = dict(c1=c1, c2=c2, offsets=index.cells.offsets, ids=index.ids, codes=index.codes, device=device,
+                  rotation=None if rot is None else rot.matrix)
         if bank is not None:
-            if bank.rot1 is not None or bank.rot2 is not None:
-                raise NotImplementedError("rotated local banks are not supported yet (SURVEY §8f f3)")
-            return cls(bank1=bank.books1, bank2=bank.books2, **kw)
+            return cls(bank1=bank.books1, bank2=bank.books2,
+                       rot1=None if bank.rot1 is None else bank.rot1.matrix,
+                       rot2=None if bank.rot2 is None else bank.rot2.matrix, **kw)
         tab = None
         if tables is not None:
             tab = (tables.coarse_norms1, tables.coarse_norms2, tables.fine_norms, tables.cross1, tables.cross2)
@@ -367,13 +382,10 @@ class DeviceIndex:
 
         rec = storage.load_index_arrays(index_path)
         tab = storage.load_tables_arrays(tables_path) if tables_path is not None else None
-        if rec["rotation"] is not None:
-            raise NotImplementedError("OPQ-rotated indexes are not supported yet (SURVEY §8f f3)")
-        kw = dict(c1=rec["c1"], c2=rec["c2"], offsets=rec["offsets"], ids=rec["ids"], codes=rec["codes"], device=device)
+        kw = dict(c1=rec["c1"], c2=rec["c2"], offsets=rec["offsets"], ids=rec["ids"], codes=rec["codes"], device=device,
+                  rotation=rec["rotation"])
         if rec["bank1"] is not None:
-            if rec["rot1"] is not None or rec["rot2"] is not None:
-                raise NotImplementedError("rotated local banks are not supported yet (SURVEY §8f f3)")
-            return cls(bank1=rec["bank1"], bank2=rec["bank2"], **kw)
+            return cls(bank1=rec["bank1"], bank2=rec["bank2"], rot1=rec["rot1"], rot2=rec["rot2"], **kw)
         return cls(books=rec["books"], tables=tab, **kw)
 
 

@@ -281,3 +281,49 @@ if __name__ == "__main__":
         make_c0()
     if "hbpq" in what:
         make_hbpq()
+
+
+def make_rot():
+    """OPQ-rotated variants (the paper's 'optimized' engines): a coarse
+    rotation learned with the coarse pair, per-half rotations in the bank."""
+    t0 = time.time()
+    D, NCOMP, N, NQ = 128, 1024, 20_000, 60
+    cent = datagen.mixture_centres(NCOMP, D)
+    base = datagen.clipped_mixture(N, D, NCOMP, datagen.SEED_BASE, cent)
+    queries = datagen.clipped_mixture(NQ, D, NCOMP, datagen.SEED_QUERIES, cent)
+    coarse = bq.train_coarse(base, 16, optimized=True, seed=0)
+    fine = bq.train_fine_global(base, coarse, 8, 64, seed=0)
+    index = bq.build_index(base, coarse, fine)
+    tables = bq.build_tables(index)
+    bank = bq.train_local_codebooks(base, coarse, 8, 64, seed=0, optimized=True)
+    hindex = bq.build_hbpq_index(base, coarse, bank)
+    out = dict(c1=coarse.book1.centroids, c2=coarse.book2.centroids, rotation=coarse.rotation.matrix,
+               books=fine.codebooks, offsets=index.cells.offsets, ids=index.ids, codes=index.codes,
+               cn1=tables.coarse_norms1, cn2=tables.coarse_norms2, fine_norms=tables.fine_norms,
+               cross1=tables.cross1, cross2=tables.cross2, bank1=bank.books1, bank2=bank.books2,
+               rot1=bank.rot1.matrix, rot2=bank.rot2.matrix, hoffsets=hindex.cells.offsets, hids=hindex.ids,
+               hcodes=hindex.codes, queries=queries.astype(np.uint8), enc_x=base[:2000].astype(np.uint8))
+    L, k = 2000, 50
+    for eng in ("fbpq", "baseline", "hbpq"):
+        res_i = np.full((NQ, k), 0xFFFFFFFF, np.uint32)
+        res_d = np.full((NQ, k), np.inf, np.float32)
+        for x in range(NQ):
+            if eng == "fbpq":
+                si, sd = bq.search_fbpq(index, tables, queries[x], L, k)
+            elif eng == "baseline":
+                si, sd = bq.search_baseline(index, queries[x], L, k)
+            else:
+                si, sd = bq.search_hbpq(hindex, queries[x], L, k)
+            res_i[x, : si.shape[0]] = si
+            res_d[x, : sd.shape[0]] = sd
+        out[f"{eng}_ids"] = res_i
+        out[f"{eng}_d"] = res_d
+    sidx = bq.build_index(base[:2000], coarse, fine)
+    shidx = bq.build_hbpq_index(base[:2000], coarse, bank)
+    out.update(enc_offsets=sidx.cells.offsets, enc_ids=sidx.ids, enc_codes=sidx.codes, enc_hcodes=shidx.codes)
+    np.savez_compressed(OUT / "rot.npz", **out)
+    print(f"rot done in {time.time() - t0:.1f}s")
+
+
+if __name__ == "__main__" and "rot" in sys.argv[1:]:
+    make_rot()

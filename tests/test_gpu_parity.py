@@ -363,3 +363,31 @@ def test_export_round_trip_through_bpqi(c0, c0_index, tmp_path):
     q = c0["queries"][:50].astype(np.float32)
     for x, y in zip(c0_index.search(q, 5000, 50).numpy(), back.search(q, 5000, 50).numpy()):
         np.testing.assert_array_equal(x, y)
+
+
+def test_rotated_variants_vs_reference(torch_cuda):
+    """OPQ-rotated coarse pair (FBPQ, Multi-D-ADC) and rotated local banks
+    (HBPQ) against the reference's own results; device encoding with
+    rotations against the reference's build_index / build_hbpq_index."""
+    from conftest import GOLDEN
+
+    from paper_1404_1831_b200 import DeviceIndex, encode
+
+    g = dict(np.load(GOLDEN / "rot.npz"))
+    tables = (g["cn1"], g["cn2"], g["fine_norms"], g["cross1"], g["cross2"])
+    dix = DeviceIndex(c1=g["c1"], c2=g["c2"], offsets=g["offsets"], ids=g["ids"], codes=g["codes"], books=g["books"],
+                      tables=tables, rotation=g["rotation"])
+    hix = DeviceIndex(c1=g["c1"], c2=g["c2"], offsets=g["hoffsets"], ids=g["hids"], codes=g["hcodes"],
+                      bank1=g["bank1"], bank2=g["bank2"], rotation=g["rotation"], rot1=g["rot1"], rot2=g["rot2"])
+    q = g["queries"].astype(np.float32)
+    for eng, ix in (("fbpq", dix), ("baseline", dix), ("hbpq", hix)):
+        d, i, c = ix.search(q, 2000, 50, eng).numpy()
+        want_c = (g[f"{eng}_ids"] != 0xFFFFFFFF).sum(1)
+        check_topk(d, i, c, g[f"{eng}_d"], g[f"{eng}_ids"], want_c, _qn(q), min_exact_frac=0.9)
+    x = g["enc_x"].astype(np.float32)
+    e = encode.build_index(x, g["c1"], g["c2"], g["books"], rotation=g["rotation"])
+    assert np.mean(np.all(e.codes.cpu().numpy() == g["enc_codes"], axis=1)) > 0.98
+    assert np.mean(e.ids.cpu().numpy().view(np.uint32) == g["enc_ids"]) > 0.98
+    h = encode.build_hbpq_index(x, g["c1"], g["c2"], g["bank1"], g["bank2"], rotation=g["rotation"], rot1=g["rot1"],
+                                rot2=g["rot2"])
+    assert np.mean(np.all(h.codes.cpu().numpy() == g["enc_hcodes"], axis=1)) > 0.98

@@ -104,3 +104,21 @@ def test_c_batch_search_within_contract(c0, oracle):
     np.testing.assert_allclose(d, want_d, rtol=1e-4)
     same = np.mean([len(set(a) & set(b)) / 100 for a, b in zip(i, want_i)])
     assert same > 0.99
+
+
+def test_rotated_variants_match_reference(oracle):
+    """OPQ-rotated coarse pair and per-half bank rotations (the paper's
+    optimized engines) reproduce the reference bit for bit."""
+    from conftest import GOLDEN
+
+    g = dict(np.load(GOLDEN / "rot.npz"))
+    tables = (g["cn1"], g["cn2"], g["fine_norms"], g["cross1"], g["cross2"])
+    idx = oracle.Index(g["c1"], g["c2"], g["offsets"], g["ids"], g["codes"], books=g["books"], tables=tables,
+                       rotation=g["rotation"])
+    hidx = oracle.Index(g["c1"], g["c2"], g["hoffsets"], g["hids"], g["hcodes"], bank1=g["bank1"], bank2=g["bank2"],
+                        rotation=g["rotation"], rot1=g["rot1"], rot2=g["rot2"])
+    q = g["queries"].astype(np.float32)
+    for eng, ix in (("fbpq", idx), ("baseline", idx), ("hbpq", hidx)):
+        d, i, c, _ = oracle.search_batch_numpy(ix, eng, q, 2000, 50)
+        np.testing.assert_array_equal(i, g[f"{eng}_ids"])
+        np.testing.assert_array_equal(d, g[f"{eng}_d"])
