@@ -152,6 +152,57 @@ def build_workload(cfg, device, rank=0):
     return dix, q, host
 
 
+def build_sharded_workload(cfg, device, rank, world):
+    """rank r holds the points with ids in [r N / W, (r+1) N / W)
+    (its own multi-index, built with id_offset) plus the GLOBAL per-cell
+    counts (one NCCL all-reduce at build time), so every rank runs the same
+    traversal under the global budget and scans only its local entries.
+    Codebooks and queries are broadcast from rank 0."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1404_1831_b200 import DeviceIndex, datagen, encode
+
+    dh = cfg["dim"] // 2
+    ds = cfg["dim"] // cfg["m"]
+    cent = datagen.mixture_centres(cfg["ncomp"], cfg["dim"])
+    centt = torch.as_tensor(cent, dtype=torch.float32, device=device)
+
+    def draw(s, e, seed):
+        return datagen.clipped_mixture_chunk(s, e, cfg["dim"], cfg["ncomp"], seed, device, centt)
+
+    c1 = torch.empty((cfg["t"], dh), device=device)
+    c2 = torch.empty((cfg["t"], dh), device=device)
+    books = torch.empty((cfg["m"], cfg["k"], ds), device=device)
+    if rank == 0:
+        train = draw(0, cfg["train"], datagen.SEED_TRAIN)
+        c1.copy_(torch.from_numpy(encode.train_kmeans(train[:, :dh].contiguous(), cfg["t"], iters=8, seed=11)))
+        c2.copy_(torch.from_numpy(encode.train_kmeans(train[:, dh:].contiguous(), cfg["t"], iters=8, seed=12)))
+        i_idx, j_idx = encode.assign_cells(train, c1.cpu().numpy(), c2.cpu().numpy())
+        disp = train - torch.cat([c1[i_idx], c2[j_idx]], 1)
+        books.copy_(torch.from_numpy(np.stack([
+            encode.train_kmeans(disp[:, p * ds:(p + 1) * ds].contiguous(), cfg["k"], iters=8, seed=20 + p)
+            for p in range(cfg["m"])])))
+    for t in (c1, c2, books):
+        dist.broadcast(t, 0)
+    c1n, c2n, booksn = c1.cpu().numpy(), c2.cpu().numpy(), books.cpu().numpy()
+    lo, hi = cfg["n"] * rank // world, cfg["n"] * (rank + 1) // world
+    local = encode.build_index_streamed(hi - lo, lambda s, e: draw(lo + s, lo + e, datagen.SEED_BASE), c1n, c2n,
+                                        booksn, id_offset=lo, device=device)
+    cnt = (local.offsets[1:].long() & 0xFFFFFFFF) - (local.offsets[:-1].long() & 0xFFFFFFFF)
+    dist.all_reduce(cnt)
+    goff = torch.zeros(cnt.numel() + 1, dtype=torch.int64, device=device)
+    torch.cumsum(cnt, 0, out=goff[1:])
+    n_global = int(goff[-1].item())
+    dix = DeviceIndex(c1=c1n, c2=c2n, offsets=local.offsets, ids=local.ids, codes=local.codes, books=booksn,
+                      tables=(local.cn1, local.cn2, local.fine_norms, local.cross1, local.cross2),
+                      global_offsets=goff.to(torch.int32), num_entries_global=n_global, device=device)
+    del local
+    q = draw(0, cfg["nq"], datagen.SEED_QUERIES)
+    dist.broadcast(q, 0)
+    return dix, q
+
+
 # -------------------------------------------------------------------- clocks
 class ClockSampler:
     """Samples SM clock and clock-event (throttle) reasons every ~5 ms via NVML
@@ -252,6 +303,8 @@ def main():
     ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--nq", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", action="store_true",
+                    help="shard the database by point id across the ranks (global budget, NCCL all-gather merge)")
     ap.add_argument("--phase-profile", action="store_true",
                     help="print per-phase cycle shares of the fused kernel (needs BPQ_LIB=...libbpq_b200_prof.so)")
     args = ap.parse_args()
@@ -263,10 +316,16 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference" and rank != 0:
         return
-    if world > 1:
+    if world > 1 or args.shard:
         import torch.distributed as dist
 
         torch.cuda.set_device(local_rank)
+        os.environ.setdefault("NCCL_DEBUG", "NONE")  # keep stdout to the one JSON line
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     device = torch.device("cuda", local_rank)
 
@@ -283,12 +342,21 @@ def main():
     if args.nq:
         cfg["nq"] = args.nq
     engine, L, k = cfg["engine"], cfg["L"], cfg["topk"]
-    dix, q, host = build_workload(cfg, device, rank)
+    searcher = None
+    if args.shard:
+        from paper_1404_1831_b200 import sharded
+
+        dix, q = build_sharded_workload(cfg, device, rank, world)
+        host = None
+        searcher = sharded.ShardedSearcher(dix, force_collective=True)
+    else:
+        dix, q, host = build_workload(cfg, device, rank)
     nq = q.shape[0]
     workload = (f"{cfg['name']}: {engine} N={dix.n:,} D={dix.dim} T={dix.t} M={dix.m}x{dix.k} "
                 f"nq={nq} L={L} k={k}")
     config = {"workload": workload, "engine": engine, "N": dix.n, "D": dix.dim, "T": dix.t, "M": dix.m,
-              "nq": nq, "L": L, "k": k, "parallelism": f"replicas{args.gpus}" if world > 1 else "single",
+              "nq": nq, "L": L, "k": k,
+              "parallelism": (f"shard{world}" if args.shard else f"replicas{args.gpus}" if world > 1 else "single"),
               "l2": "flushed between timed steps (256 MiB write)"}
     metric = "queries/s (batched search at fixed L, k)"
 
@@ -362,21 +430,32 @@ def main():
 
         dist.barrier()
     torch.cuda.synchronize()
+    sev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
     with ClockSampler(local_rank) as clk:
         for s in range(args.steps):
             flush.fill_(s & 0xFF)  # L2 flush, outside the event pair
-            dix.search(q, L, k, engine, out=out, workspace=ws, stage_events=evs[s])
+            if searcher is not None:  # local search + NCCL all-gather + device merge
+                sev[s][0].record(stream)
+                searcher.search(q, L, k, engine, workspace=ws, stage_events=evs[s])
+                sev[s][1].record(stream)
+            else:
+                dix.search(q, L, k, engine, out=out, workspace=ws, stage_events=evs[s])
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    step_ms = [evs[s][0].elapsed_time(evs[s][3]) for s in range(args.steps)]
+    if searcher is not None:
+        step_ms = [sev[s][0].elapsed_time(sev[s][1]) for s in range(args.steps)]
+    else:
+        step_ms = [evs[s][0].elapsed_time(evs[s][3]) for s in range(args.steps)]
     stage_ms = np.array([[evs[s][i].elapsed_time(evs[s][i + 1]) for i in range(3)] for s in range(args.steps)])
     t_ms = float(np.sum(step_ms))
     if world > 1:
         tt = torch.tensor([t_ms], device=device)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_ms = float(tt.item())
-    value = world * nq * args.steps / (t_ms / 1e3)
+    # replicas: every rank answers its own batch; shard: all ranks answer one batch
+    qmul = 1 if args.shard else world
+    value = qmul * nq * args.steps / (t_ms / 1e3)
 
     # end to end through the public API with host buffers
     q_host = q.cpu().pin_memory()
@@ -390,14 +469,19 @@ def main():
         flush.fill_((s + 7) & 0xFF)
         e0.record(stream)
         q_dev.copy_(q_host, non_blocking=True)
-        dix.search(q_dev, L, k, engine, out=out, workspace=ws)
-        od_h.copy_(out.dists, non_blocking=True)
-        oi_h.copy_(out.ids, non_blocking=True)
-        oc_h.copy_(out.counts, non_blocking=True)
+        res = (searcher.search(q_dev, L, k, engine, workspace=ws) if searcher is not None
+               else dix.search(q_dev, L, k, engine, out=out, workspace=ws))
+        od_h.copy_(res.dists, non_blocking=True)
+        oi_h.copy_(res.ids, non_blocking=True)
+        oc_h.copy_(res.counts, non_blocking=True)
         e1.record(stream)
         torch.cuda.synchronize()
         e2e_ms += e0.elapsed_time(e1)
-    e2e_v = world * nq * args.steps / (e2e_ms / 1e3)
+    if world > 1:
+        tt = torch.tensor([e2e_ms], device=device)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    e2e_v = qmul * nq * args.steps / (e2e_ms / 1e3)
 
     # roofline of the fused traversal+scan kernel ((M+4) B per candidate + 16 B per popped cell)
     search_ms = float(np.mean(stage_ms[:, 2]))
@@ -411,7 +495,8 @@ def main():
         pass
     line = {
         "metric": metric, "value": value, "unit": "queries/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong" if args.shard else "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded BASELINE.json generator)",
         "config": config,
         "codes_scanned_per_s": world * ncand * args.steps / (t_ms / 1e3),
@@ -424,17 +509,17 @@ def main():
                      "peak_source": HBM_PEAK_SRC, "alg_bytes_per_launch": alg_bytes},
         "e2e": {"value": e2e_v, "unit": "queries/s", "h2d_bytes_per_step": int(q.numel() * 4),
                 "d2h_bytes_per_step": int(nq * k * 8 + nq * 4)},
-        "gpu_launches": launches_per_step(dix, engine) * args.steps,
+        "gpu_launches": (launches_per_step(dix, engine) + (1 if searcher is not None else 0)) * args.steps,
         "clocks": clk.summary(),
     }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and host is not None:
         try:
             line["cpu_baseline"] = cpu_baseline(host(), engine, q.cpu().numpy(), L, k)
         except Exception as e:  # the baseline is reported, never required
             line["cpu_baseline"] = {"error": repr(e)}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if world > 1 or args.shard:
         import torch.distributed as dist
 
         dist.destroy_process_group()

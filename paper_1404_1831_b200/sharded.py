@@ -95,9 +95,10 @@ class ShardedSearcher:
     search, all-gathers the [nq, k] lists over the process group and merges
     them on the device; every rank returns the merged result."""
 
-    def __init__(self, local, group=None):
+    def __init__(self, local, group=None, force_collective=False):
         self.local = local
         self.group = group
+        self.force_collective = force_collective  # exercise the exchange even on one rank
 
     def search(self, queries, L: int, k: int, engine: str = "fbpq", **kw) -> SearchResult:
         import torch
@@ -105,7 +106,7 @@ class ShardedSearcher:
 
         res = self.local.search(queries, L, k, engine, **kw)
         world = dist.get_world_size(self.group)
-        if world == 1:
+        if world == 1 and not self.force_collective:
             return res
         nq = res.dists.shape[0]
         gd = torch.empty((world, nq, k), dtype=torch.float32, device=res.dists.device)

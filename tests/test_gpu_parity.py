@@ -391,3 +391,26 @@ def test_rotated_variants_vs_reference(torch_cuda):
     h = encode.build_hbpq_index(x, g["c1"], g["c2"], g["bank1"], g["bank2"], rotation=g["rotation"], rot1=g["rot1"],
                                 rot2=g["rot2"])
     assert np.mean(np.all(h.codes.cpu().numpy() == g["enc_hcodes"], axis=1)) > 0.98
+
+
+def test_sharded_searcher_nccl_single_rank(c0, c0_index):
+    """ShardedSearcher over a real NCCL group (world 1, exchange forced):
+    local search -> all_gather_into_tensor -> device merge == local result."""
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1404_1831_b200 import sharded
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29547")
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        q = c0["queries"][:64].astype(np.float32)
+        got = sharded.ShardedSearcher(c0_index, force_collective=True).search(q, 10_000, 100).numpy()
+        want = c0_index.search(q, 10_000, 100).numpy()
+        for x, y in zip(got, want):
+            np.testing.assert_array_equal(x, y)
+    finally:
+        dist.destroy_process_group()
