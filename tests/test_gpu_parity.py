@@ -414,3 +414,48 @@ def test_sharded_searcher_nccl_single_rank(c0, c0_index):
             np.testing.assert_array_equal(x, y)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_fuzz_small_configs_vs_oracle(torch_cuda, oracle, seed):
+    """Randomised small indexes: T, M (incl. the generic runtime-M path),
+    K, quantised data (distance and key ties), empty cells, L from 1 to
+    beyond N, k beyond the candidates; dense and sparse traversal; every
+    engine.  Contract of SURVEY §8c(ii) against the oracle."""
+    from paper_1404_1831_b200 import DeviceIndex
+
+    rng = np.random.default_rng(1000 + seed)
+    t = int(rng.integers(2, 40)) if seed % 5 else int(rng.integers(1030, 1400))  # >1024: partial sort
+    m = int(rng.choice([2, 4, 6, 8]))
+    dim = m * int(rng.integers(1, 5)) * 2
+    kk = int(rng.integers(2, 64))
+    n = int(rng.integers(50, 4000))
+    quant = seed % 2 == 0
+    base = rng.normal(size=(n, dim)).astype(np.float32)
+    if quant:
+        base = np.round(base * 2) / 2
+    c1 = base[rng.choice(n, t, replace=t > n), : dim // 2].copy()
+    c2 = base[rng.choice(n, t, replace=t > n), dim // 2 :].copy()
+    books = (0.3 * rng.normal(size=(m, kk, dim // m))).astype(np.float32)
+    if quant:
+        books = np.round(books * 4) / 4
+    off, ids, codes = oracle.build_index(base, c1, c2, books, id_offset=int(rng.integers(0, 1000)))
+    bank1 = (0.3 * rng.normal(size=(t, m // 2, kk, dim // m))).astype(np.float32)
+    bank2 = (0.3 * rng.normal(size=(t, m // 2, kk, dim // m))).astype(np.float32)
+    idx = oracle.Index(c1, c2, off, ids, codes, books=books)
+    hidx = oracle.Index(c1, c2, off, ids, codes, bank1=bank1, bank2=bank2)
+    q = rng.normal(size=(24, dim)).astype(np.float32)
+    if quant:
+        q = np.round(q * 2) / 2
+    for lists in (False, True):
+        dix = DeviceIndex(c1=c1, c2=c2, offsets=off, ids=ids, codes=codes, books=books, tables=idx.tables,
+                          cell_lists=lists)
+        hix = DeviceIndex(c1=c1, c2=c2, offsets=off, ids=ids, codes=codes, bank1=bank1, bank2=bank2,
+                          cell_lists=lists)
+        Ls = (1, int(rng.integers(2, n)), n, 3 * n) if t <= 1024 else (1, int(rng.integers(2, n // 4)))
+        for L in Ls:
+            k = int(rng.integers(1, 200))
+            for eng, di, oi in (("fbpq", dix, idx), ("baseline", dix, idx), ("hbpq", hix, hidx)):
+                wd, wi, wc, _ = oracle.search_batch_numpy(oi, eng, q, L, k)
+                d, i, c = di.search(q, L, k, eng).numpy()
+                check_topk(d, i, c, wd, wi, wc, _qn(q), min_exact_frac=0.5)
