@@ -471,6 +471,7 @@ struct Query {
     const float *d1, *d2;
     const float *u1, *u2;    // unsorted half-distances (codeword-keyed entries)
     float *erot;             // [NT][D] rotated displacement rows of the current chunk (HBPQ)
+    int lut_i, lut_j;        // coarse codewords the two LUT halves were built for (-1: none)
     bool cw;                 // list entries hold codewords (i, j) instead of positions (a, b)
     int T, P, M;
     int tp1, tp2;              // valid sorted prefix per half (partial sort), block-uniform
@@ -495,6 +496,7 @@ struct Query {
         u2 = A.ru2 ? A.ru2 + q * T : nullptr;
         cw = false;
         erot = nullptr;
+        lut_i = lut_j = -1;
         ncand = 0;
         popped = 0;
     }
@@ -574,13 +576,21 @@ struct Query {
         (void)pv;
         const int M2 = M / 2;
         const int K = A.K;
-        for (int idx = threadIdx.x; idx < M * K; idx += NT) {
-            const int p = idx / K, c = idx - p * K;
-            const float x = p < M2 ? __ldg(A.cross1 + ((size_t)oi * M2 + p) * K + c)
-                                   : __ldg(A.cross2 + ((size_t)oj * M2 + (p - M2)) * K + c);
-            lut[idx] = __fadd_rn(tab[idx], __fmul_rn(2.f, x));
+        // each half of the LUT depends on one coarse codeword only: rebuild a
+        // half only when the cell's row (or column) changed since the last cell
+        const int lo_idx = oi == lut_i ? M2 * K : 0;
+        const int hi_idx = oj == lut_j ? M2 * K : M * K;
+        if (lo_idx < hi_idx) {
+            for (int idx = lo_idx + threadIdx.x; idx < hi_idx; idx += NT) {
+                const int p = idx / K, c = idx - p * K;
+                const float x = p < M2 ? __ldg(A.cross1 + ((size_t)oi * M2 + p) * K + c)
+                                       : __ldg(A.cross2 + ((size_t)oj * M2 + (p - M2)) * K + c);
+                lut[idx] = __fadd_rn(tab[idx], __fmul_rn(2.f, x));
+            }
+            __syncthreads();
         }
-        __syncthreads();
+        lut_i = oi;
+        lut_j = oj;
         // kLutUnroll codes per thread per round keep 2x the bytes in flight
         for (uint32_t e0 = 0; e0 < lc; e0 += NT * kLutUnroll) {
             uint32_t w[kLutUnroll][4];
