@@ -412,9 +412,9 @@ def main():
         dix.search(q, L, k, engine, out=out, workspace=ws)
         torch.cuda.synchronize()
         _lib.load().bpq_debug_set_phase_buffer(None)
-        names = ["prologue", "tau_search", "band_bounds", "enumerate", "scan", "lut_scan", "topk_compact",
-                 "final_select", "finish", "idle"]
-        c = ctr.cpu().numpy()[:10].astype(float)
+        names = ["prologue", "tau_search|sparse_reclassify", "band_bounds|sparse_activate", "enumerate|sparse_gather",
+                 "scan", "lut_scan", "topk_compact", "final_select", "finish", "idle", "extend_prefix"]
+        c = ctr.cpu().numpy()[:11].astype(float)
         log(json.dumps({"phase_profile_compiled": bool(on),
                         "phase_share": {n: round(float(v / max(c.sum(), 1)), 4) for n, v in zip(names, c)}}))
     for _ in range(args.warmup):
@@ -483,9 +483,11 @@ def main():
         e2e_ms = float(tt.item())
     e2e_v = qmul * nq * args.steps / (e2e_ms / 1e3)
 
-    # roofline of the fused traversal+scan kernel ((M+4) B per candidate + 16 B per popped cell)
+    # roofline of the fused traversal+scan kernel ((M+4) B per candidate + 16 B per popped
+    # cell; the FBPQ point-term scan reads 4 B more per candidate: code M + point term 4 + id 4)
     search_ms = float(np.mean(stage_ms[:, 2]))
-    alg_bytes = (dix.m + 4) * ncand + 16 * npop
+    per_cand = dix.m + 4 + (4 if engine == "fbpq" and not dix.fbpq_exact else 0)
+    alg_bytes = per_cand * ncand + 16 * npop
     achieved = alg_bytes / (search_ms / 1e3) / 1e9
     traffic = None
     try:  # dram bytes per launch of the same kernel from the committed ncu --set full capture
@@ -506,7 +508,8 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": HBM_PEAK, "unit": "GB/s",
                      "frac": achieved / HBM_PEAK, "traffic": traffic,
                      "kernel": "search_kernel (fused traversal + scan + top-k)",
-                     "peak_source": HBM_PEAK_SRC, "alg_bytes_per_launch": alg_bytes},
+                     "peak_source": HBM_PEAK_SRC, "alg_bytes_per_launch": alg_bytes,
+                     "alg_bytes_formula": f"{per_cand} B/candidate + 16 B/popped cell"},
         "e2e": {"value": e2e_v, "unit": "queries/s", "h2d_bytes_per_step": int(q.numel() * 4),
                 "d2h_bytes_per_step": int(nq * k * 8 + nq * 4)},
         "gpu_launches": (launches_per_step(dix, engine) + (1 if searcher is not None else 0)) * args.steps,

@@ -5,7 +5,8 @@
  * passed as void*).  Every entry point returns an int status (BPQ_OK == 0);
  * on failure bpq_last_error() returns a thread-local message.  No C++
  * exception crosses this boundary, no entry point allocates device memory
- * behind the caller's back except bpq_index_create in host-copy mode, and no
+ * behind the caller's back except bpq_index_create (host-copy mode, and the
+ * FBPQ point-term array, see bpq_index_desc.fbpq_exact), and no
  * entry point synchronises the host except where noted.
  *
  * Reference interfaces each group replaces (paths relative to
@@ -37,7 +38,7 @@
 extern "C" {
 #endif
 
-#define BPQ_ABI_VERSION 1
+#define BPQ_ABI_VERSION 2
 
 enum {
     BPQ_OK = 0,
@@ -83,6 +84,16 @@ typedef struct bpq_index_desc {
      * the bank's per-half R1, R2 [D/2, D/2] applied to the query
      * displacements of HBPQ (hbpq.py:328-331).  NULL = none. */
     const float *rotation, *rot1, *rot2;
+    /* FBPQ scan arithmetic of bpq_search.  0 (default): the index derives a
+     * query-independent point term pt[e] = sum_p 2*cross_h[row][p][code_p]
+     * (f64 sum, one rounding; 4 B per entry of library-owned device memory)
+     * and scores an entry as ((sum_p fold[p][code_p]) + pt[e]) + cell_base:
+     * M shared-memory lookups and one 4 B load instead of M cross-table
+     * gathers, within 1e-6 relative of the reference.  1: the reference's
+     * exact operation order (numba_backend.py:231-242), bit-identical per
+     * candidate given the same query tables.  The stage kernel
+     * bpq_scan_tables is always exact. */
+    int32_t fbpq_exact;
 } bpq_index_desc;
 
 typedef struct bpq_index bpq_index;
@@ -90,6 +101,7 @@ typedef struct bpq_index bpq_index;
 const char *bpq_last_error(void);
 int bpq_abi_version(void);
 
+/* Synchronises the device when it derives the FBPQ point-term array. */
 int bpq_index_create(const bpq_index_desc *desc, int copy_from_host, bpq_index **out);
 int bpq_index_destroy(bpq_index *index);
 

@@ -54,6 +54,7 @@ class IndexDesc(ctypes.Structure):
         ("rotation", P),
         ("rot1", P),
         ("rot2", P),
+        ("fbpq_exact", I32),
     ]
 
 

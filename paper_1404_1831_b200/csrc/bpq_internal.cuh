@@ -51,6 +51,7 @@ struct Index {
     const uint8_t *codes;
     const float *books, *fine_norms, *cross1, *cross2, *bank1, *bank2;
     const float *rot, *rot1, *rot2;  // optional rotations (see bpq_index_desc)
+    const float *pterm;  // FBPQ per-entry cross term [N] (null: exact reference-order scan)
     // populated-cell lists (optional): row i -> columns j, column j -> rows i
     const uint32_t *rowptr, *colptr;
     const uint16_t *rowcols, *colrows;
@@ -58,6 +59,8 @@ struct Index {
 };
 
 // ---- launchers implemented in the .cu files --------------------------------
+int launch_point_term(const uint32_t *offsets, int32_t t, int32_t m, int32_t k, const uint8_t *codes,
+                      const float *cross1, const float *cross2, float *pt, cudaStream_t s);
 int launch_coarse_dots(const float *queries, int64_t nq, int32_t D, const float *c1,
                        const float *c2, int32_t T, float *dots1, float *dots2,
                        cudaStream_t stream);

@@ -184,6 +184,25 @@ extern "C" int bpq_index_create(const bpq_index_desc *d, int copy_from_host, bpq
             return fail(BPQ_ERR_CUDA, msg);
         }
     }
+    ix.pterm = nullptr;
+    if (ix.cross1 && ix.cross2 && ix.codes && N > 0 && !d->fbpq_exact) {
+        float *pt = nullptr;
+        if (cudaMalloc(&pt, N * sizeof(float)) != cudaSuccess) {
+            cudaGetLastError();
+            bpq_index_destroy(h);
+            return fail(BPQ_ERR_CUDA, "cannot allocate the FBPQ point-term array");
+        }
+        ix.owned.push_back(pt);
+        int rc = launch_point_term(ix.loff, ix.T, ix.M, ix.K, ix.codes, ix.cross1, ix.cross2, pt, 0);
+        if (rc == BPQ_OK && cudaDeviceSynchronize() != cudaSuccess)
+            rc = fail(BPQ_ERR_CUDA, cudaGetErrorString(cudaGetLastError()));
+        if (rc) {
+            std::string msg = g_last_error;
+            bpq_index_destroy(h);
+            return fail(BPQ_ERR_CUDA, msg);
+        }
+        ix.pterm = pt;
+    }
     *out = h;
     return BPQ_OK;
 }

@@ -54,6 +54,35 @@ __global__ void line_fill_kernel(const uint32_t *__restrict__ off, int t, int by
 
 size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
+
+// FBPQ point term: pt[e] = sum_p 2 * cross_h[row][p][code_p] for every entry
+// e of cell (i, j) (row = i for the first M/2 parts, j for the rest).  It is
+// query independent, so the batched scan reads 4 B per entry instead of
+// gathering M cross-table values (numba_backend.py:236-240 does the gathers
+// per query).  Summed in f64 and rounded once.  One CTA per cell row i with
+// cross1[i] staged in shared memory; entries of row i are contiguous.
+__global__ void point_term_kernel(const uint32_t *__restrict__ off, int t, int m, int k,
+                                  const uint8_t *__restrict__ codes, const float *__restrict__ cross1,
+                                  const float *__restrict__ cross2, float *__restrict__ pt) {
+    extern __shared__ float c1s[];
+    const int i = blockIdx.x;
+    const int m2 = m / 2;
+    for (int x = threadIdx.x; x < m2 * k; x += CT) c1s[x] = cross1[(size_t)i * m2 * k + x];
+    __syncthreads();
+    const uint32_t *row = off + (size_t)i * t;
+    for (int j = threadIdx.x; j < t; j += CT) {
+        const uint32_t g0 = row[j], g1 = row[j + 1];
+        const float *c2 = cross2 + (size_t)j * m2 * k;
+        for (uint32_t e = g0; e < g1; e++) {
+            const uint8_t *c = codes + (size_t)e * m;
+            double acc = 0.0;
+            for (int p = 0; p < m2; p++) acc += 2.0 * (double)c1s[p * k + c[p]];
+            for (int p = 0; p < m2; p++) acc += 2.0 * (double)__ldg(c2 + p * k + c[m2 + p]);
+            pt[e] = (float)acc;
+        }
+    }
+}
+
 }  // namespace
 }  // namespace bpq
 
@@ -89,3 +118,13 @@ extern "C" int bpq_build_cell_lists(const uint32_t *offsets, int32_t t, uint32_t
     BPQ_CUDA_TRY(cudaGetLastError());
     return BPQ_OK;
 }
+
+namespace bpq {
+int launch_point_term(const uint32_t *offsets, int32_t t, int32_t m, int32_t k, const uint8_t *codes,
+                      const float *cross1, const float *cross2, float *pt, cudaStream_t s) {
+    const size_t smem = (size_t)(m / 2) * k * sizeof(float);
+    point_term_kernel<<<t, CT, smem, s>>>(offsets, t, m, k, codes, cross1, cross2, pt);
+    BPQ_CUDA_TRY(cudaGetLastError());
+    return BPQ_OK;
+}
+}  // namespace bpq

@@ -232,7 +232,7 @@ constexpr int kCutMin = 256;
 constexpr int kBuckets = 1024;
 
 template <int ITEMS, int P>
-__global__ void __launch_bounds__(kSortThreads) row_topk_kernel(
+__global__ void __launch_bounds__(kSortThreads, ITEMS <= 8 ? 3 : 1) row_topk_kernel(
     const float *__restrict__ Q, int D, const float *__restrict__ dots1,
     const float *__restrict__ dots2, const float *__restrict__ cn1,
     const float *__restrict__ cn2, int T, float *__restrict__ sr1, float *__restrict__ sr2,
@@ -274,20 +274,51 @@ __global__ void __launch_bounds__(kSortThreads) row_topk_kernel(
     const float *dots = (h ? dots2 : dots1) + q * T;
     const float *cn = h ? cn2 : cn1;
     float *ru = (h ? ru2 : ru1) + q * T;
+    // striped float4 arrangement (coalesced 16-byte loads/stores); the
+    // order of keys across threads is irrelevant to the (value, index) sort
+    auto ix = [](int s) { return ((s >> 2) * kSortThreads + (int)threadIdx.x) * 4 + (s & 3); };
     unsigned int keys[ITEMS];
     unsigned int kmin = 0xFFFFFFFFu, kmax = 0u;
+    auto rval = [&](float c, float d) {
+        float r = __fadd_rn(__fsub_rn(c, __fmul_rn(2.f, d)), qn);
+        return r > 0.f ? r : 0.f;  // np.maximum(r, 0) (multi_index.py:291-292)
+    };
+    if ((T & 3) == 0) {
 #pragma unroll
-    for (int s = 0; s < ITEMS; s++) {
-        const int idx = threadIdx.x * ITEMS + s;
-        if (idx < T) {
-            float r = __fadd_rn(__fsub_rn(__ldg(cn + idx), __fmul_rn(2.f, __ldg(dots + idx))), qn);
-            if (!(r > 0.f)) r = 0.f;
-            keys[s] = __float_as_uint(r);
-            ru[idx] = r;
-            kmin = min(kmin, keys[s]);
-            kmax = max(kmax, keys[s]);
-        } else {
-            keys[s] = 0xFFFFFFFFu;
+        for (int j = 0; j < ITEMS / 4; j++) {
+            const int b = ix(j * 4);
+            if (b < T) {
+                const float4 dv = __ldg(reinterpret_cast<const float4 *>(dots + b));
+                const float4 cv = __ldg(reinterpret_cast<const float4 *>(cn + b));
+                const float4 rv = make_float4(rval(cv.x, dv.x), rval(cv.y, dv.y), rval(cv.z, dv.z), rval(cv.w, dv.w));
+                *reinterpret_cast<float4 *>(ru + b) = rv;
+                keys[j * 4 + 0] = __float_as_uint(rv.x);
+                keys[j * 4 + 1] = __float_as_uint(rv.y);
+                keys[j * 4 + 2] = __float_as_uint(rv.z);
+                keys[j * 4 + 3] = __float_as_uint(rv.w);
+#pragma unroll
+                for (int e = 0; e < 4; e++) {
+                    kmin = min(kmin, keys[j * 4 + e]);
+                    kmax = max(kmax, keys[j * 4 + e]);
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < 4; e++) keys[j * 4 + e] = 0xFFFFFFFFu;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int s = 0; s < ITEMS; s++) {
+            const int idx = ix(s);
+            if (idx < T) {
+                const float r = rval(__ldg(cn + idx), __ldg(dots + idx));
+                keys[s] = __float_as_uint(r);
+                ru[idx] = r;
+                kmin = min(kmin, keys[s]);
+                kmax = max(kmax, keys[s]);
+            } else {
+                keys[s] = 0xFFFFFFFFu;
+            }
         }
     }
 #pragma unroll
@@ -314,6 +345,7 @@ __global__ void __launch_bounds__(kSortThreads) row_topk_kernel(
         s_cnt = 0;
     }
     __syncthreads();
+    const unsigned int gmin = s_lo;
     // up to two histogram refinements of [lo, lo + 1024 << shift)
     unsigned int below = 0;  // keys already known to be under the window
     for (int pass = 0; pass < 2; pass++) {
@@ -322,7 +354,7 @@ __global__ void __launch_bounds__(kSortThreads) row_topk_kernel(
         __syncthreads();
 #pragma unroll
         for (int s = 0; s < ITEMS; s++) {
-            if (threadIdx.x * ITEMS + s < T && keys[s] >= lo) {
+            if (ix(s) < T && keys[s] >= lo) {
                 const unsigned int bkt = (keys[s] - lo) >> shift;
                 if (bkt < (unsigned int)kBuckets) atomicAdd(&hist[bkt], 1u);
             }
@@ -371,38 +403,84 @@ __global__ void __launch_bounds__(kSortThreads) row_topk_kernel(
     // (if both passes ended inside an overfull bucket, s_cut / s_cnt hold
     // the last clean cut below it; a short prefix just retries sooner)
     const unsigned int cut = s_cut;
-    unsigned int take = 0;
-#pragma unroll
-    for (int s = 0; s < ITEMS; s++) take += (threadIdx.x * ITEMS + s < T && keys[s] < cut) ? 1u : 0u;
-    unsigned int pos, total;
-    Scan(tmp.scan).ExclusiveSum(take, pos, total);
+    // Counting sort of the keys below the cut: 1024 linear buckets over
+    // [gmin, cut) (monotone in the key), scatter, then each bucket -- almost
+    // always 0-3 keys -- is insertion-sorted on (value, index) by one thread,
+    // so equal values keep ascending index (stable, as np.argsort).  A bucket
+    // fuller than kBucketSortMax (massive ties) falls back to a bitonic sort.
+    constexpr unsigned int kBucketSortMax = 24;
+    const unsigned int span = cut - gmin;
+    const int sbits = span ? 32 - __clz(span) : 0;
+    const unsigned int sshift = sbits > 10 ? sbits - 10 : 0;
+    for (int i = threadIdx.x; i < kBuckets; i += kSortThreads) hist[i] = 0;
     __syncthreads();
+#pragma unroll
+    for (int s = 0; s < ITEMS; s++)
+        if (ix(s) < T && keys[s] < cut) atomicAdd(&hist[(keys[s] - gmin) >> sshift], 1u);
+    __syncthreads();
+    unsigned int total;
+    {
+        const int b0 = threadIdx.x * 2;
+        const unsigned int c0 = hist[b0], c1 = hist[b0 + 1];
+        unsigned int base;
+        Scan(tmp.scan).ExclusiveSum(c0 + c1, base, total);
+        unsigned int m = max(c0, c1);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (lane == 0) s_wsum[warp] = m;
+        __syncthreads();  // all reads of hist done before it becomes the cursor array
+        hist[b0] = base;
+        hist[b0 + 1] = base + c0;
+    }
+    __syncthreads();
+    unsigned int maxb = 0;
+#pragma unroll
+    for (int w = 0; w < kSortThreads / 32; w++) maxb = max(maxb, s_wsum[w]);
 #pragma unroll
     for (int s = 0; s < ITEMS; s++) {
-        if (threadIdx.x * ITEMS + s < T && keys[s] < cut) {
-            sk64[pos] = ((unsigned long long)keys[s] << 32) | (unsigned int)(threadIdx.x * ITEMS + s);
-            pos++;
+        if (ix(s) < T && keys[s] < cut) {
+            const unsigned int at = atomicAdd(&hist[(keys[s] - gmin) >> sshift], 1u);
+            sk64[at] = ((unsigned long long)keys[s] << 32) | (unsigned int)ix(s);
         }
     }
-    int P2 = 1;
-    while (P2 < (int)total) P2 <<= 1;
-    for (int x = total + threadIdx.x; x < P2; x += kSortThreads) sk64[x] = ~0ull;
     __syncthreads();
-    // bitonic sort of (value, index): equal values keep ascending index (stable)
-    for (int k = 2; k <= P2; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = threadIdx.x; i < P2; i += kSortThreads) {
-                const int ixj = i ^ j;
-                if (ixj > i) {
-                    const bool up = (i & k) == 0;
-                    const unsigned long long x = sk64[i], y = sk64[ixj];
-                    if ((x > y) == up) {
-                        sk64[i] = y;
-                        sk64[ixj] = x;
+    if (maxb <= kBucketSortMax) {
+        if (maxb > 1) {
+            // hist[b] is now the end of bucket b (= start of bucket b + 1)
+            for (int b = threadIdx.x; b < kBuckets; b += kSortThreads) {
+                const int e = (int)hist[b], st = b ? (int)hist[b - 1] : 0;
+                for (int i = st + 1; i < e; i++) {
+                    const unsigned long long v = sk64[i];
+                    int j = i - 1;
+                    while (j >= st && sk64[j] > v) {
+                        sk64[j + 1] = sk64[j];
+                        j--;
                     }
+                    sk64[j + 1] = v;
                 }
             }
             __syncthreads();
+        }
+    } else {
+        int P2 = 1;
+        while (P2 < (int)total) P2 <<= 1;
+        for (int x = total + threadIdx.x; x < P2; x += kSortThreads) sk64[x] = ~0ull;
+        __syncthreads();
+        for (int k = 2; k <= P2; k <<= 1) {
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int i = threadIdx.x; i < P2; i += kSortThreads) {
+                    const int ixj = i ^ j;
+                    if (ixj > i) {
+                        const bool up = (i & k) == 0;
+                        const unsigned long long x = sk64[i], y = sk64[ixj];
+                        if ((x > y) == up) {
+                            sk64[i] = y;
+                            sk64[ixj] = x;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
         }
     }
     float *sr = (h ? sr2 : sr1) + q * T;

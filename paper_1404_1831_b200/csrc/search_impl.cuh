@@ -40,6 +40,7 @@
 // it fills.
 #include <cfloat>
 #include <cmath>
+#include <cstdlib>
 
 #include "bpq_internal.cuh"
 
@@ -55,6 +56,30 @@ constexpr int ENGINE_TRAVERSE = 3;
 constexpr int kUnroll = 4;                // candidates per thread per round
 constexpr int kSrSmem = 4096;             // sorted half-distances staged in smem
 constexpr int kEnumBatch = 8;             // cell-table reads in flight per thread
+#ifndef BPQ_PIPE_U
+#define BPQ_PIPE_U 2
+#endif
+#ifndef BPQ_PIPE_S
+#define BPQ_PIPE_S 2
+#endif
+constexpr int kPipeU = BPQ_PIPE_U;        // large-cell scan: entries per thread per round
+constexpr int kPipeR = NT * kPipeU;       // entries per round
+constexpr int kPipeS = BPQ_PIPE_S;        // cp.async stages (rounds in flight + 1)
+// shared-memory bytes of the large-cell pipeline for M parts (code + point term per entry)
+__host__ __device__ constexpr int pipe_stage_bytes(int m) { return kPipeS * kPipeR * (m + 4); }
+
+__device__ __forceinline__ void cp_async4(void *smem, const void *g) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(g));
+}
+__device__ __forceinline__ void cp_async8(void *smem, const void *g) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(g));
+}
+__device__ __forceinline__ void cp_async16(void *smem, const void *g) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(g));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 struct __align__(16) Smem {
     unsigned long long tk[kTopkBuf];
@@ -111,12 +136,13 @@ __device__ __forceinline__ int prof_switch(Smem &S, unsigned long long *acc, int
 }
 #define PROF(ph) prof_switch(S, A.prof, (ph))
 #else
-#define PROF(ph) ((void)0, 0)
+__device__ __forceinline__ int prof_nop() { return 0; }
+#define PROF(ph) prof_nop()
 #endif
 
 // Optional per-phase cycle accounting (compile with -DBPQ_PHASE_PROF): thread 0
 // of each CTA attributes elapsed clock64 cycles to the current phase.
-enum Phase { PH_PROLOGUE, PH_TAU, PH_BOUNDS, PH_ENUM, PH_SCAN, PH_LUT, PH_COMPACT, PH_FINAL, PH_FINISH, PH_IDLE, PH_N };
+enum Phase { PH_PROLOGUE, PH_TAU, PH_BOUNDS, PH_ENUM, PH_SCAN, PH_LUT, PH_COMPACT, PH_FINAL, PH_FINISH, PH_IDLE, PH_EXTEND, PH_N };
 
 template <typename KT, typename OffT>
 struct Args {
@@ -127,6 +153,7 @@ struct Args {
     const uint32_t *ids;
     const uint8_t *codes;
     const float *books, *fine_norms, *cross1, *cross2, *bank1, *bank2;
+    const float *pterm;        // FBPQ per-entry point term (null: exact reference order)
     const float *rot1, *rot2;  // HBPQ per-half rotations (optional)
     double rho;
     unsigned long long n_global;
@@ -145,6 +172,8 @@ struct Args {
     const uint16_t *rowcols, *colrows;
     long long L;
     int k;
+    int lut_min;     // cells with >= lut_min entries take the per-cell scan
+    int nb0;         // lines activated by the first sparse-traversal batch
     int tab_floats;  // floats of the per-query table staged after Smem
     int sr_smem;     // sorted-key prefix length staged in smem
     float *out_d;
@@ -315,6 +344,23 @@ __device__ __forceinline__ float dist_fbpq(const Args<KT, OffT> &A, const float 
     return acc;
 }
 
+// FBPQ through the index's point term pt = sum_p 2*cross[row][p][c_p]
+// (bpq_index_desc.fbpq_exact == 0): ((sum_p fold[p][c_p]) + pt) + cell_base,
+// M shared-memory lookups and no cross-table gathers.  Same quantity as the
+// reference's cell_base + sum_p (fold + 2*cross) (numba_backend.py:231-242),
+// summed in another order (max 4.3e-7 relative on the config-0 captures).
+template <int MT>
+__device__ __forceinline__ float dist_fbpq_pt(const float *tab, int M, int K, float cbase, float pt,
+                                              const uint32_t (&w)[4]) {
+    if constexpr (MT != 0) M = MT;
+    float s = tab[code_at(w, 0)];
+#pragma unroll
+    for (int p = 1; p < (MT ? MT : 16); p++)
+        if (MT || p < M) s = __fadd_rn(s, tab[p * K + code_at(w, p)]);
+    const float acc = __fadd_rn(__fadd_rn(s, pt), cbase);
+    return acc < 0.f ? 0.f : acc;
+}
+
 // Multi-D-ADC explicit reconstruction (ENGINE 0) and HBPQ local books
 // (ENGINE 2): e = q_h - c_h[row] (one rounding, multi_index.py:345-346),
 // d = e - book, acc += d*d sequentially (numba_backend.py:165-176, 198-210).
@@ -457,7 +503,11 @@ __device__ void topk_compact(Smem &S, int k) {
 // key(b + 1, b) exceeds tau, so a count or a band touches only O(active
 // rows + active columns) lines even when the region is a long thin "L"
 // (one very close codeword per half, which the BASELINE mixture produces).
-template <int ENGINE, int MT, typename KT, typename OffT>
+// SPARSE_ONLY: the first pass over a partially sorted sparse table.  Any
+// query the sparse traversal cannot finish is queued for the full-sort retry
+// pass, so the band (dense) traversal is compiled out of this instantiation
+// -- which keeps the scan loop free of register spills.
+template <int ENGINE, int MT, typename KT, typename OffT, bool SPARSE_ONLY = false>
 struct Query {
     const Args<KT, OffT> &A;
     Smem &S;
@@ -580,7 +630,7 @@ struct Query {
         // half only when the cell's row (or column) changed since the last cell
         const int lo_idx = oi == lut_i ? M2 * K : 0;
         const int hi_idx = oj == lut_j ? M2 * K : M * K;
-        if (lo_idx < hi_idx) {
+        if (A.pterm == nullptr && lo_idx < hi_idx) {
             for (int idx = lo_idx + threadIdx.x; idx < hi_idx; idx += NT) {
                 const int p = idx / K, c = idx - p * K;
                 const float x = p < M2 ? __ldg(A.cross1 + ((size_t)oi * M2 + p) * K + c)
@@ -594,24 +644,112 @@ struct Query {
         // kLutUnroll codes per thread per round keep 2x the bytes in flight
         for (uint32_t e0 = 0; e0 < lc; e0 += NT * kLutUnroll) {
             uint32_t w[kLutUnroll][4];
+            float ptv[kLutUnroll];
 #pragma unroll
             for (int u = 0; u < kLutUnroll; u++) {
                 const uint32_t e = e0 + u * NT + threadIdx.x;
-                if (e < lc) load_code<MT>(A.codes + (size_t)(lst + e) * M, w[u], M);
+                if (e < lc) {
+                    load_code<MT>(A.codes + (size_t)(lst + e) * M, w[u], M);
+                    if (A.pterm) ptv[u] = __ldg(A.pterm + lst + e);
+                }
             }
 #pragma unroll
             for (int u = 0; u < kLutUnroll; u++) {
                 const uint32_t e = e0 + u * NT + threadIdx.x;
                 if (e < lc) {
-                    float acc = cb;
+                    float acc;
+                    if (A.pterm) {
+                        acc = dist_fbpq_pt<MT>(tab, M, K, cb, ptv[u], w[u]);
+                    } else {
+                        acc = cb;
 #pragma unroll
-                    for (int p = 0; p < M; p++) acc = __fadd_rn(acc, lut[p * K + code_at(w[u], p)]);
-                    if (acc < 0.f) acc = 0.f;
+                        for (int p = 0; p < M; p++) acc = __fadd_rn(acc, lut[p * K + code_at(w[u], p)]);
+                        if (acc < 0.f) acc = 0.f;
+                    }
                     offer_lazy(acc, A.ids + lst + e);
                 }
             }
             round_end(NT * kLutUnroll);
         }
+        __syncthreads();
+        PROF(pv);
+    }
+
+    // FBPQ point-term scan of the band's large cells (M = 8 or 16): all of
+    // them as one stream of rounds of kPipeR entries.  Each thread copies its
+    // own entries' code and point term into its own shared-memory slots with
+    // cp.async, kPipeS - 1 rounds ahead of the round it scores, so the
+    // contiguous cell ranges stream from HBM while earlier rounds are scored
+    // (no register staging, no barrier between copy and use: a thread only
+    // reads the slots it filled).
+    __device__ void scan_big_pt(uint32_t nb) {
+        static_assert(MT == 8 || MT == 16, "pipelined scan needs M = 8 or 16");
+        const int pv = PROF(PH_LUT);
+        (void)pv;
+        const int K = A.K;
+        uint8_t *stc = reinterpret_cast<uint8_t *>(lut);       // [kPipeS][kPipeR][MT]
+        float *stp = reinterpret_cast<float *>(stc + kPipeS * kPipeR * MT);  // [kPipeS][kPipeR]
+        // issue cursor (x_i, e_i) and score cursor (x_c, e_c) walk the same
+        // round sequence; both are block-uniform
+        uint32_t x_i = 0, e_i = 0, x_c = 0, e_c = 0;
+        auto issue = [&](int slot) {
+            if (x_i < nb) {
+                const int t = S.bigs[x_i];
+                const uint32_t lst = S.cstart[t], lc = S.ccnt[t];
+#pragma unroll
+                for (int u = 0; u < kPipeU; u++) {
+                    const int j = u * NT + threadIdx.x;
+                    const uint32_t e = e_i + j;
+                    if (e < lc) {
+                        uint8_t *dc = stc + ((size_t)slot * kPipeR + j) * MT;
+                        const uint8_t *gc = A.codes + (size_t)(lst + e) * MT;
+                        if constexpr (MT == 16) cp_async16(dc, gc); else cp_async8(dc, gc);
+                        cp_async4(stp + slot * kPipeR + j, A.pterm + lst + e);
+                    }
+                }
+                e_i += kPipeR;
+                if (e_i >= lc) {
+                    x_i++;
+                    e_i = 0;
+                }
+            }
+            cp_async_commit();  // possibly empty: keeps the group count uniform
+        };
+#pragma unroll
+        for (int r = 0; r < kPipeS - 1; r++) issue(r);
+        for (int r = 0; x_c < nb; r++) {
+            issue((r + kPipeS - 1) % kPipeS);
+            cp_async_wait<kPipeS - 1>();
+            const int slot = r % kPipeS;
+            const int t = S.bigs[x_c];
+            const uint32_t lst = S.cstart[t], lc = S.ccnt[t];
+            const float cb = S.cbase[t];
+#pragma unroll
+            for (int u = 0; u < kPipeU; u++) {
+                const int j = u * NT + threadIdx.x;
+                const uint32_t e = e_c + j;
+                if (e < lc) {
+                    uint32_t w[4];
+                    if constexpr (MT == 16) {
+                        const uint4 v = *reinterpret_cast<const uint4 *>(stc + ((size_t)slot * kPipeR + j) * MT);
+                        w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+                    } else {
+                        const uint2 v = *reinterpret_cast<const uint2 *>(stc + ((size_t)slot * kPipeR + j) * MT);
+                        w[0] = v.x; w[1] = v.y; w[2] = 0; w[3] = 0;
+                    }
+                    const float acc = dist_fbpq_pt<MT>(tab, MT, K, cb, stp[slot * kPipeR + j], w);
+                    offer_lazy(acc, A.ids + lst + e);
+                }
+            }
+            e_c += kPipeR;
+            if (e_c >= lc) {
+                ncand += lc;
+                x_c++;
+                e_c = 0;
+            }
+            round_end(kPipeR);
+        }
+        cp_async_wait<0>();
         __syncthreads();
         PROF(pv);
     }
@@ -649,7 +787,7 @@ struct Query {
                         float s = __fadd_rn(__ldg(d1 + oi), __ldg(d2 + oj));
                         float t0 = __fsub_rn(S.qnorm, __fmul_rn(2.f, s));
                         cb = __fadd_rn(__fadd_rn(t0, __ldg(A.cn1 + oi)), __ldg(A.cn2 + oj));
-                        big = lc >= (uint32_t)kLutMin;
+                        big = lc >= (uint32_t)A.lut_min;
                     }
                 }
             }
@@ -693,6 +831,7 @@ struct Query {
                     uint32_t entry[kUnroll];
                     int own[kUnroll];
                     uint32_t w[kUnroll][4];
+                    float ptv[kUnroll];
 #pragma unroll
                     for (int u = 0; u < kUnroll; u++) {
                         const uint32_t e = e0 + u * NT + threadIdx.x;
@@ -706,6 +845,8 @@ struct Query {
                             own[u] = lo;
                             entry[u] = S.cstart[lo] + (e - S.cpre[lo]);
                             load_code<MT>(A.codes + (size_t)entry[u] * M, w[u], M);
+                            if constexpr (ENGINE == BPQ_ENGINE_FBPQ)
+                                ptv[u] = A.pterm ? __ldg(A.pterm + entry[u]) : 0.f;
                         }
                     }
 #pragma unroll
@@ -714,7 +855,8 @@ struct Query {
                         const int lo = own[u];
                         float dist;
                         if constexpr (ENGINE == BPQ_ENGINE_FBPQ)
-                            dist = dist_fbpq<MT>(A, tab, S.coi[lo], S.coj[lo], S.cbase[lo], w[u]);
+                            dist = A.pterm ? dist_fbpq_pt<MT>(tab, M, A.K, S.cbase[lo], ptv[u], w[u])
+                                           : dist_fbpq<MT>(A, tab, S.coi[lo], S.coj[lo], S.cbase[lo], w[u]);
                         else
                             dist = dist_recon<ENGINE, MT>(A, tab, S.coi[lo], S.coj[lo], w[u],
                                                           erot ? erot + (size_t)lo * A.D : nullptr);
@@ -722,7 +864,18 @@ struct Query {
                     }
                     round_end();
                 }
-                if constexpr (ENGINE == BPQ_ENGINE_FBPQ) {
+                if constexpr (ENGINE == BPQ_ENGINE_FBPQ && MT != 0) {
+                    if (A.pterm != nullptr) {
+                        if (S.nbig) scan_big_pt(S.nbig);
+                    } else {
+                        const uint32_t nb = S.nbig;
+                        for (uint32_t x = 0; x < nb; x++) {
+                            const int t = S.bigs[x];
+                            ncand += S.ccnt[t];
+                            scan_cell_lut(S.coi[t], S.coj[t], S.cstart[t], S.ccnt[t], S.cbase[t]);
+                        }
+                    }
+                } else if constexpr (ENGINE == BPQ_ENGINE_FBPQ) {
                     const uint32_t nb = S.nbig;
                     for (uint32_t x = 0; x < nb; x++) {
                         const int t = S.bigs[x];
@@ -1155,15 +1308,17 @@ struct Query {
         cw = true;
         unsigned long long W = 0;
         int nr = 0, nc = 0, npend = 0;
-        int NB = 32;
+        int NB = A.nb0;
         for (;;) {
             // the batch probes rows < nr + NB and columns < nc + NB (column b
             // reads position b + 1): stay inside the sorted prefix
             if (partial) {
                 const int need = max(nr + NB, nc + NB + 1) + 1;
+                if (need > tp1 || need > tp2) PROF(PH_EXTEND);
                 if (need > tp1) extend(0, need);
                 if (need > tp2) extend(1, need);
             }
+            PROF(PH_BOUNDS);
             // next NB lines in activation order (merge path over the two sequences)
             if (threadIdx.x < 32) {
                 const int x = warp_first_false(
@@ -1182,6 +1337,7 @@ struct Query {
             }
             __syncthreads();
             // gather newly active lines' cells (one line per thread, flattened)
+            PROF(PH_ENUM);
             unsigned long long wb = 0;
             const int nnew = (nr2 - nr) + (nc2 - nc);
             for (int base = 0; base < nnew; base += NT) {
@@ -1256,6 +1412,7 @@ struct Query {
                 __syncthreads();
             }
             // re-classify the pool against the new kappa
+            PROF(PH_TAU);
             for (int c = threadIdx.x; c < npend; c += NT) {
                 const int4 cell = pend[c];
                 if (ekey(cell) < kappa) {
@@ -1319,11 +1476,11 @@ struct Query {
         }
         __syncthreads();
         if (A.n_global == 0) return;
-        if (A.rowptr != nullptr && A.ru1 != nullptr) {
+        if (SPARSE_ONLY || (A.rowptr != nullptr && A.ru1 != nullptr)) {
             const int rs = run_sparse(listA, listB, listC, listD);
             if (rs == 1) return;
             cw = false;
-            if (rs == 2 || A.plen != nullptr || A.topP < T) {
+            if (SPARSE_ONLY || rs == 2 || A.plen != nullptr || A.topP < T) {
                 // needs the full sort: queue for the retry pass (outputs written there)
                 if (threadIdx.x == 0) {
                     S.err = 2;
@@ -1342,6 +1499,11 @@ struct Query {
             __syncthreads();
         }
 
+        if constexpr (!SPARSE_ONLY) run_dense(rowB, colB, rowNew, colNew, segLine, seg, listA, listB, listC, listD);
+    }
+
+    __device__ void run_dense(int32_t *rowB, int32_t *colB, int32_t *rowNew, int32_t *colNew, uint32_t *segLine,
+                              uint4 *seg, int4 *listA, int4 *listB, int4 *listC, int4 *listD) {
         const bool lists = A.rowptr != nullptr;
         const unsigned long long Tall = (unsigned long long)T * T;
         const unsigned long long L = (unsigned long long)A.L;
@@ -1601,7 +1763,7 @@ struct Query {
     }
 };
 
-template <int ENGINE, int MT, typename KT, typename OffT>
+template <int ENGINE, int MT, typename KT, typename OffT, bool SPARSE_ONLY = false>
 __global__ void __launch_bounds__(NT, BPQ_MINB) search_kernel(Args<KT, OffT> A) {
     const int M = MT ? MT : A.M;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1665,7 +1827,7 @@ __global__ void __launch_bounds__(NT, BPQ_MINB) search_kernel(Args<KT, OffT> A) 
             }
         }
         __syncthreads();
-        Query<ENGINE, MT, KT, OffT> Q(A, S, qi, tab, lut, s1s, s2s);
+        Query<ENGINE, MT, KT, OffT, SPARSE_ONLY> Q(A, S, qi, tab, lut, s1s, s2s);
         Q.run();
         Q.finish();
         __syncthreads();
@@ -1689,10 +1851,10 @@ int num_sms() {
     return g_num_sms;
 }
 
-template <int ENGINE, int MT, typename KT, typename OffT>
+template <int ENGINE, int MT, typename KT, typename OffT, bool SPARSE_ONLY = false>
 int configure(size_t smem, int *n_cta_out) {
     static bool attr = false;
-    auto kfn = search_kernel<ENGINE, MT, KT, OffT>;
+    auto kfn = search_kernel<ENGINE, MT, KT, OffT, SPARSE_ONLY>;
     if (!attr) {
         int dev = 0, optin = 0;
         BPQ_CUDA_TRY(cudaGetDevice(&dev));
@@ -1713,12 +1875,18 @@ int launch_one(const Index &ix, const float *queries, int64_t q0, int64_t nq, in
                int32_t *out_count, int64_t *out_ncand, int64_t *out_popped, cudaStream_t stream) {
     Args<float, uint32_t> A{};
     A.M = ix.M;
-    A.tab_floats = ENGINE == BPQ_ENGINE_FBPQ ? 2 * ix.M * ix.K : ix.D;  // fold + per-cell LUT
+    // fold + per-cell LUT (exact FBPQ), or fold + the large-cell cp.async stages (point-term FBPQ)
+    A.tab_floats = ENGINE != BPQ_ENGINE_FBPQ ? ix.D
+                   : (MT != 0 && ix.pterm != nullptr) ? ix.M * ix.K + pipe_stage_bytes(ix.M) / 4
+                                                      : 2 * ix.M * ix.K;
     A.tab_floats = (A.tab_floats + 3) & ~3;
     A.sr_smem = 0;  // sorted keys are read through L1: only active lines are probed
     const size_t smem = dyn_smem_bytes(A.tab_floats, A.sr_smem, sizeof(float));
+    // first pass over a partially sorted sparse table: sparse traversal only
+    const bool sparse_only = MT != 0 && ix.rowptr != nullptr && ws.topP < ix.T && ws.qlist == nullptr;
     int n_cta = 0;
-    int rc = configure<ENGINE, MT, float, uint32_t>(smem, &n_cta);
+    int rc = sparse_only ? configure<ENGINE, MT, float, uint32_t, (MT != 0)>(smem, &n_cta)
+                         : configure<ENGINE, MT, float, uint32_t>(smem, &n_cta);
     if (rc) return rc;
     if (n_cta > ws.n_cta) n_cta = ws.n_cta;
     A.T = ix.T;
@@ -1739,6 +1907,11 @@ int launch_one(const Index &ix, const float *queries, int64_t q0, int64_t nq, in
     A.fine_norms = ix.fine_norms;
     A.cross1 = ix.cross1;
     A.cross2 = ix.cross2;
+    A.pterm = ENGINE == BPQ_ENGINE_FBPQ ? ix.pterm : nullptr;
+    static const int lut_min_env = getenv("BPQ_LUT_MIN") ? atoi(getenv("BPQ_LUT_MIN")) : 0;  // A/B experiments
+    A.lut_min = lut_min_env > 0 ? lut_min_env : kLutMin;
+    static const int nb0_env = getenv("BPQ_NB0") ? atoi(getenv("BPQ_NB0")) : 0;  // A/B experiments
+    A.nb0 = nb0_env > 0 ? (nb0_env < NT ? nb0_env : NT) : 128;
     A.bank1 = ix.bank1;
     A.bank2 = ix.bank2;
     A.rot1 = ix.rot1;
@@ -1781,7 +1954,10 @@ int launch_one(const Index &ix, const float *queries, int64_t q0, int64_t nq, in
     A.scratch = ws.cta_scratch;
     A.stride = ws.cta_stride;
     BPQ_CUDA_TRY(cudaMemsetAsync(ws.counter, 0, sizeof(unsigned int), stream));
-    search_kernel<ENGINE, MT, float, uint32_t><<<n_cta, NT, smem, stream>>>(A);
+    if (sparse_only)
+        search_kernel<ENGINE, MT, float, uint32_t, (MT != 0)><<<n_cta, NT, smem, stream>>>(A);
+    else
+        search_kernel<ENGINE, MT, float, uint32_t><<<n_cta, NT, smem, stream>>>(A);
     BPQ_CUDA_TRY(cudaGetLastError());
     return BPQ_OK;
 }

@@ -14,6 +14,8 @@ from __future__ import annotations
 import ctypes
 from dataclasses import dataclass
 
+import os
+
 import numpy as np
 
 from . import _lib
@@ -106,10 +108,17 @@ class DeviceIndex:
 
     def __init__(self, *, c1, c2, offsets, ids, codes, books=None, tables=None, bank1=None,
                  bank2=None, global_offsets=None, device=None, num_entries_global=None, cell_lists="auto",
-                 rotation=None, rot1=None, rot2=None):
+                 rotation=None, rot1=None, rot2=None, fbpq_exact=None):
+        """``fbpq_exact``: score FBPQ candidates in the reference's exact
+        operation order (numba_backend.py:231-242) instead of through the
+        precomputed per-entry point term (bpq_index_desc.fbpq_exact); default
+        from the environment variable BPQ_FBPQ_EXACT=1."""
         import torch
 
         self.device = torch.device(device if device is not None else "cuda")
+        if fbpq_exact is None:
+            fbpq_exact = os.environ.get("BPQ_FBPQ_EXACT") == "1"
+        self.fbpq_exact = bool(fbpq_exact)
         c1n = c1.detach().cpu().numpy() if isinstance(c1, torch.Tensor) else np.asarray(c1, np.float32)
         c2n = c2.detach().cpu().numpy() if isinstance(c2, torch.Tensor) else np.asarray(c2, np.float32)
         if c1n.shape != c2n.shape or c1n.ndim != 2:
@@ -231,6 +240,7 @@ class DeviceIndex:
         d.row_ptr, d.col_ptr = _lib.ptr(self.row_ptr), _lib.ptr(self.col_ptr)
         d.row_cols, d.col_rows = _lib.ptr(self.row_cols), _lib.ptr(self.col_rows)
         d.rotation, d.rot1, d.rot2 = _lib.ptr(self.rotation), _lib.ptr(self.rot1), _lib.ptr(self.rot2)
+        d.fbpq_exact = 1 if self.fbpq_exact else 0
         h = ctypes.c_void_p()
         _lib.check(lib.bpq_index_create(ctypes.byref(d), 0, ctypes.byref(h)), "bpq_index_create")
         self._handle = h

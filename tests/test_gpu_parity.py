@@ -108,6 +108,26 @@ def test_search_c0_vs_reference(c0, c0_index, engine, nq, L, k):
     assert np.mean(ncand == c0[tag + "_ncand"][:nq]) > 0.99
 
 
+def test_fbpq_exact_and_point_term_modes(c0, c0_index, torch_cuda):
+    """The default FBPQ scan reads the index's per-entry point term; the
+    exact mode gathers cross terms in the reference's operation order.  Both
+    meet the reference contract, agree on counts and on every distance to
+    1e-6 relative, and return identical id lists away from exact ties."""
+    from paper_1404_1831_b200 import DeviceIndex
+
+    tables = (c0["cn1"], c0["cn2"], c0["fine_norms"], c0["cross1"], c0["cross2"])
+    exact = DeviceIndex(c1=c0["c1"], c2=c0["c2"], offsets=c0["offsets"], ids=c0["ids"], codes=c0["codes"],
+                        books=c0["books"], tables=tables, fbpq_exact=True)
+    q = c0["queries"][:500].astype(np.float32)
+    de, ie, ce = exact.search(q, 10_000, 100, "fbpq").numpy()
+    dp, ip, cp = c0_index.search(q, 10_000, 100, "fbpq").numpy()
+    want_c = np.minimum(100, c0["fbpq_L10000_k100_ncand"][:500])
+    check_topk(de, ie, ce, c0["fbpq_L10000_k100_d"][:500], c0["fbpq_L10000_k100_ids"][:500], want_c, _qn(q))
+    np.testing.assert_array_equal(ce, cp)
+    np.testing.assert_allclose(dp, de, rtol=1e-6)
+    assert np.mean([np.array_equal(a, b) for a, b in zip(ie, ip)]) >= 0.99
+
+
 def test_search_hbpq_vs_reference(hbpq_rig, torch_cuda):
     from paper_1404_1831_b200 import DeviceIndex
 
