@@ -109,6 +109,7 @@ struct __align__(16) Smem {
     int cnt_nc;
     double mtau[NW];
     unsigned long long mcnt[NW];
+    unsigned long long tor[NW];  // top-k compaction: per-warp OR of the buffered keys
     uint32_t nbig;
     int err;
     int prof_ph;
@@ -419,9 +420,37 @@ __device__ __forceinline__ float dist_recon(const Args<KT, OffT> &A, const float
 __device__ void topk_compact(Smem &S, int k) {
     const uint32_t n = S.ntk;
     if ((int)n <= k) return;
-    unsigned long long prefix = 0, pmask = 0;
+    // bits shared by every buffered key (AND == OR) need no histogram pass:
+    // start at the digit holding the highest differing bit
+    unsigned long long ka = ~0ull, ko = 0ull;
+    for (uint32_t i = threadIdx.x; i < n; i += NT) {
+        ka &= S.tk[i];
+        ko |= S.tk[i];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        ka &= __shfl_xor_sync(0xffffffffu, ka, o);
+        ko |= __shfl_xor_sync(0xffffffffu, ko, o);
+    }
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) {
+        S.red[threadIdx.x >> 5] = ka;
+        S.tor[threadIdx.x >> 5] = ko;
+    }
+    __syncthreads();
+    ka = ~0ull;
+    ko = 0ull;
+#pragma unroll
+    for (int w = 0; w < NW; w++) {
+        ka &= S.red[w];
+        ko |= S.tor[w];
+    }
+    const int hb = 63 - __clzll((long long)(ka ^ ko));  // keys are unique: ka != ko
+    const int top = (hb / 8) * 8;
+    unsigned long long pmask = top >= 56 ? 0ull : ~0ull << (top + 8);
+    unsigned long long prefix = ka & pmask;
     uint32_t rank = (uint32_t)k;  // 1-based rank of the wanted key among matches
-    for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int shift = top; shift >= 0; shift -= 8) {
         for (int i = threadIdx.x; i < 256; i += NT) S.hist_c[i] = 0;
         __syncthreads();
         for (uint32_t i = threadIdx.x; i < n; i += NT) {
@@ -1048,7 +1077,30 @@ struct Query {
                     S.sidx[c] = (uint16_t)c;
                 }
                 __syncthreads();
-                bitonic_sort_cells(S, P2);
+                if (n <= NT) {
+                    // rank sort: (key, lin) pairs are unique (lin is the cell)
+                    unsigned long long kc = 0;
+                    uint32_t lc = 0;
+                    int rank = 0;
+                    const int c = threadIdx.x;
+                    if (c < n) {
+                        kc = S.skey[c];
+                        lc = S.slin[c];
+                        for (int y = 0; y < n; y++) {
+                            const unsigned long long ky = S.skey[y];
+                            rank += (ky < kc || (ky == kc && S.slin[y] < lc)) ? 1 : 0;
+                        }
+                    }
+                    __syncthreads();
+                    if (c < n) {
+                        S.skey[rank] = kc;
+                        S.slin[rank] = lc;
+                        S.sidx[rank] = (uint16_t)c;
+                    }
+                    __syncthreads();
+                } else {
+                    bitonic_sort_cells(S, P2);
+                }
                 // first sorted position where the running count reaches need
                 if (threadIdx.x == 0) S.nlist = 0xFFFFFFFFu;
                 unsigned long long run = 0;
@@ -1738,22 +1790,32 @@ struct Query {
         }
         topk_compact(S, k);
         uint32_t n = S.ntk;
-        int P2 = 1;
-        while (P2 < (int)n) P2 <<= 1;
-        for (int i = threadIdx.x; i < P2; i += NT)
-            if (i >= (int)n) S.tk[i] = ~0ull;
-        __syncthreads();
-        bitonic_sort_u64(S.tk, P2);
         int cnt = (int)min((unsigned long long)k, ncand);
-        for (int x = threadIdx.x; x < k; x += NT) {
-            if (x < cnt) {
+        if (n <= 512) {
+            // keys are unique: each key's rank is its output position
+            for (int x = threadIdx.x; x < (int)n; x += NT) {
+                const unsigned long long kx = S.tk[x];
+                int rank = 0;
+                for (uint32_t y = 0; y < n; y++) rank += S.tk[y] < kx ? 1 : 0;
+                A.out_d[qo * k + rank] = __uint_as_float((uint32_t)(kx >> 32));
+                A.out_ids[qo * k + rank] = (uint32_t)kx;
+            }
+        } else {
+            int P2 = 1;
+            while (P2 < (int)n) P2 <<= 1;
+            for (int i = threadIdx.x; i < P2; i += NT)
+                if (i >= (int)n) S.tk[i] = ~0ull;
+            __syncthreads();
+            bitonic_sort_u64(S.tk, P2);
+            for (int x = threadIdx.x; x < cnt; x += NT) {
                 unsigned long long kk = S.tk[x];
                 A.out_d[qo * k + x] = __uint_as_float((uint32_t)(kk >> 32));
                 A.out_ids[qo * k + x] = (uint32_t)kk;
-            } else {
-                A.out_d[qo * k + x] = INFINITY;
-                A.out_ids[qo * k + x] = 0xFFFFFFFFu;
             }
+        }
+        for (int x = cnt + threadIdx.x; x < k; x += NT) {
+            A.out_d[qo * k + x] = INFINITY;
+            A.out_ids[qo * k + x] = 0xFFFFFFFFu;
         }
         if (threadIdx.x == 0) {
             A.out_count[qo] = cnt;
@@ -1911,7 +1973,8 @@ int launch_one(const Index &ix, const float *queries, int64_t q0, int64_t nq, in
     static const int lut_min_env = getenv("BPQ_LUT_MIN") ? atoi(getenv("BPQ_LUT_MIN")) : 0;  // A/B experiments
     A.lut_min = lut_min_env > 0 ? lut_min_env : kLutMin;
     static const int nb0_env = getenv("BPQ_NB0") ? atoi(getenv("BPQ_NB0")) : 0;  // A/B experiments
-    A.nb0 = nb0_env > 0 ? (nb0_env < NT ? nb0_env : NT) : 128;
+    // first sparse-traversal batch: small budgets stop within a few lines
+    A.nb0 = nb0_env > 0 ? (nb0_env < NT ? nb0_env : NT) : budget <= 2000 ? 32 : budget <= 5000 ? 64 : 128;
     A.bank1 = ix.bank1;
     A.bank2 = ix.bank2;
     A.rot1 = ix.rot1;
