@@ -28,7 +28,6 @@ int fail(int code, const std::string &msg);
 
 // Tunables of the fused traversal + scan + top-k kernel.
 constexpr int kSearchThreads = 256;     // threads per CTA (one CTA per query at a time)
-constexpr int kTopkBuf = 2048;          // per-CTA top-k candidate buffer (u64 keys)
 constexpr int kLutUnroll = 4;           // codes per thread per round in the LUT scan
 constexpr int kMaxK = 1024;             // largest k the engine accepts
 constexpr int kSortCap = 512;           // final-band cells sorted in shared memory

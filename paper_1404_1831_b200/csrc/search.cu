@@ -204,9 +204,11 @@ int launch_traverse_stage(const double *sr1, const double *sr2, const int32_t *o
         return BPQ_OK;
     }
     Args<double, int64_t> A{};
-    A.tab_floats = 4;
+    A.tab_floats = 4 + kSortBytes / 4;  // the sort arrays live after the (unused) table
     A.sr_smem = t < kSrSmem ? (int)t : kSrSmem;
-    const size_t smem = dyn_smem_bytes(A.tab_floats, A.sr_smem, sizeof(double));
+    A.tkcap = 0;
+    A.tk_off = (int)tk_offset(A.tab_floats, A.sr_smem, sizeof(double));
+    const size_t smem = dyn_smem_bytes(A.tab_floats, A.sr_smem, sizeof(double), 0);
     int n_cta = 0;
     int rc = configure<ENGINE_TRAVERSE, 2, double, int64_t>(smem, &n_cta);
     if (rc) return rc;

@@ -17,7 +17,7 @@ int search_grid_ctas(int engine, int M) {
     (void)engine;
     (void)M;
     int n = 0;
-    if (configure<BPQ_ENGINE_FBPQ, 8, float, uint32_t>(dyn_smem_bytes(4, 0, 4), &n)) return -1;
+    if (configure<BPQ_ENGINE_FBPQ, 8, float, uint32_t>(dyn_smem_bytes(4, 0, 4, topk_capacity(1)), &n)) return -1;
     return n;
 }
 

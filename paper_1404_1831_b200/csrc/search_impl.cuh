@@ -38,6 +38,7 @@
 // id, i.e. (dist asc, id asc) as select_top, multi_index.py:326-339) are
 // appended to a shared-memory buffer that is bitonic-compacted to k when
 // it fills.
+#include <algorithm>
 #include <cfloat>
 #include <cmath>
 #include <cstdlib>
@@ -67,6 +68,7 @@ constexpr int kPipeR = NT * kPipeU;       // entries per round
 constexpr int kPipeS = BPQ_PIPE_S;        // cp.async stages (rounds in flight + 1)
 // shared-memory bytes of the large-cell pipeline for M parts (code + point term per entry)
 __host__ __device__ constexpr int pipe_stage_bytes(int m) { return kPipeS * kPipeR * (m + 4); }
+constexpr int kSortBytes = kSortCap * (8 + 4 + 2);  // skey + slin + sidx
 
 __device__ __forceinline__ void cp_async4(void *smem, const void *g) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(g));
@@ -82,8 +84,6 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 struct __align__(16) Smem {
-    unsigned long long tk[kTopkBuf];
-    unsigned long long skey[kSortCap];
     uint32_t cpre[NT + 1];
     int32_t coi[NT];
     int32_t coj[NT];
@@ -91,8 +91,6 @@ struct __align__(16) Smem {
     float cbase[NT];
     uint32_t ccnt[NT];
     uint16_t bigs[NT];
-    uint32_t slin[kSortCap];
-    uint16_t sidx[kSortCap];
     uint32_t hist_w[256];
     uint32_t hist_c[256];
     unsigned long long red[NW];
@@ -175,6 +173,8 @@ struct Args {
     int k;
     int lut_min;     // cells with >= lut_min entries take the per-cell scan
     int nb0;         // lines activated by the first sparse-traversal batch
+    int tkcap;       // top-k buffer capacity (keys) in dynamic shared memory
+    int tk_off;      // its byte offset in dynamic shared memory
     int tab_floats;  // floats of the per-query table staged after Smem
     int sr_smem;     // sorted-key prefix length staged in smem
     float *out_d;
@@ -261,24 +261,24 @@ __device__ __forceinline__ void bitonic_sort_u64(unsigned long long *a, int n) {
 }
 
 // sort (skey, slin) ascending carrying sidx; n power of two
-__device__ __forceinline__ void bitonic_sort_cells(Smem &S, int n) {
+__device__ __forceinline__ void bitonic_sort_cells(unsigned long long *skey, uint32_t *slin, uint16_t *sidx, int n) {
     for (int k = 2; k <= n; k <<= 1) {
         for (int j = k >> 1; j > 0; j >>= 1) {
             for (int i = threadIdx.x; i < n; i += NT) {
                 int ixj = i ^ j;
                 if (ixj > i) {
                     bool up = (i & k) == 0;
-                    unsigned long long ka = S.skey[i], kb = S.skey[ixj];
-                    uint32_t la = S.slin[i], lb = S.slin[ixj];
+                    unsigned long long ka = skey[i], kb = skey[ixj];
+                    uint32_t la = slin[i], lb = slin[ixj];
                     bool gt = (ka > kb) || (ka == kb && la > lb);
                     if (gt == up) {
-                        S.skey[i] = kb;
-                        S.skey[ixj] = ka;
-                        S.slin[i] = lb;
-                        S.slin[ixj] = la;
-                        uint16_t t = S.sidx[i];
-                        S.sidx[i] = S.sidx[ixj];
-                        S.sidx[ixj] = t;
+                        skey[i] = kb;
+                        skey[ixj] = ka;
+                        slin[i] = lb;
+                        slin[ixj] = la;
+                        uint16_t t = sidx[i];
+                        sidx[i] = sidx[ixj];
+                        sidx[ixj] = t;
                     }
                 }
             }
@@ -417,15 +417,15 @@ __device__ __forceinline__ float dist_recon(const Args<KT, OffT> &A, const float
 // is in the low word).  An MSB-first radix select on the 64-bit keys finds
 // the k-th smallest in a few 256-bin histogram passes, then the survivors
 // are compacted to the front and the admission threshold becomes that key.
-__device__ void topk_compact(Smem &S, int k) {
+__device__ void topk_compact(Smem &S, unsigned long long *__restrict__ tk, int k) {
     const uint32_t n = S.ntk;
     if ((int)n <= k) return;
     // bits shared by every buffered key (AND == OR) need no histogram pass:
     // start at the digit holding the highest differing bit
     unsigned long long ka = ~0ull, ko = 0ull;
     for (uint32_t i = threadIdx.x; i < n; i += NT) {
-        ka &= S.tk[i];
-        ko |= S.tk[i];
+        ka &= tk[i];
+        ko |= tk[i];
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -454,7 +454,7 @@ __device__ void topk_compact(Smem &S, int k) {
         for (int i = threadIdx.x; i < 256; i += NT) S.hist_c[i] = 0;
         __syncthreads();
         for (uint32_t i = threadIdx.x; i < n; i += NT) {
-            const unsigned long long key = S.tk[i];
+            const unsigned long long key = tk[i];
             if ((key & pmask) == prefix) atomicAdd(&S.hist_c[(key >> shift) & 0xFF], 1u);
         }
         __syncthreads();
@@ -492,7 +492,7 @@ __device__ void topk_compact(Smem &S, int k) {
         if (S.tcnt == 1u) {
             // a single key carries this prefix: it is the k-th smallest
             for (uint32_t i = threadIdx.x; i < n; i += NT)
-                if ((S.tk[i] & pmask) == prefix) S.tkey = S.tk[i];
+                if ((tk[i] & pmask) == prefix) S.tkey = tk[i];
             __syncthreads();
             prefix = S.tkey;
             break;
@@ -508,11 +508,11 @@ __device__ void topk_compact(Smem &S, int k) {
     }
     __syncthreads();
     for (int i = threadIdx.x; i < k; i += NT)
-        if (S.tk[i] > kth) S.holes[atomicAdd(&S.nholes, 1u)] = (uint16_t)i;
+        if (tk[i] > kth) S.holes[atomicAdd(&S.nholes, 1u)] = (uint16_t)i;
     __syncthreads();
     for (uint32_t i = k + threadIdx.x; i < n; i += NT) {
-        const unsigned long long key = S.tk[i];
-        if (key <= kth) S.tk[S.holes[atomicAdd(&S.tcnt, 1u)]] = key;
+        const unsigned long long key = tk[i];
+        if (key <= kth) tk[S.holes[atomicAdd(&S.tcnt, 1u)]] = key;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -545,6 +545,12 @@ struct Query {
     const KT *s1s, *s2s;     // smem prefixes [0, P)
     const float *tab;        // smem per-query table (fold or query vector)
     float *lut;              // smem per-cell lookup table (FBPQ)
+    unsigned long long *tk;  // smem top-k buffer [A.tkcap]
+    // final-band / prefix-extension sort arrays [kSortCap]: they alias the
+    // per-cell LUT or cp.async stages, which are dead whenever they are live
+    unsigned long long *skey;
+    uint32_t *slin;
+    uint16_t *sidx;
     const int32_t *o1, *o2;  // sorted position -> codeword
     const int32_t *p1, *p2;  // codeword -> sorted position
     const float *d1, *d2;
@@ -558,8 +564,11 @@ struct Query {
     unsigned long long popped;
 
     __device__ Query(const Args<KT, OffT> &a, Smem &s, int64_t q, const float *tab_, float *lut_,
-                     const KT *s1, const KT *s2)
-        : A(a), S(s), qi(q), s1s(s1), s2s(s2), tab(tab_), lut(lut_) {
+                     const KT *s1, const KT *s2, unsigned long long *tk_)
+        : A(a), S(s), qi(q), s1s(s1), s2s(s2), tab(tab_), lut(lut_), tk(tk_) {
+        skey = reinterpret_cast<unsigned long long *>(lut_);
+        slin = reinterpret_cast<uint32_t *>(skey + kSortCap);
+        sidx = reinterpret_cast<uint16_t *>(slin + kSortCap);
         T = A.T;
         M = MT ? MT : A.M;
         P = A.sr_smem;
@@ -625,7 +634,7 @@ struct Query {
         const unsigned long long kk = ((unsigned long long)canon_bits(dist) << 32) | id;
         if (kk < S.thr) {
             uint32_t pos = atomicAdd(&S.ntk, 1u);
-            S.tk[pos] = kk;
+            tk[pos] = kk;
         }
     }
 
@@ -639,9 +648,9 @@ struct Query {
 
     __device__ __forceinline__ void round_end(int cap = NT * kUnroll) {
         __syncthreads();
-        if (S.ntk > (uint32_t)(kTopkBuf - cap)) {
+        if (S.ntk > (uint32_t)(A.tkcap - cap)) {
             const int pv = PROF(PH_COMPACT);
-            topk_compact(S, A.k);
+            topk_compact(S, tk, A.k);
             PROF(pv);
             (void)pv;
         }
@@ -1068,13 +1077,13 @@ struct Query {
                 for (int c = threadIdx.x; c < P2; c += NT) {
                     if (c < n) {
                         int4 e = cur[c];
-                        S.skey[c] = (unsigned long long)__double_as_longlong(ekey(e));
-                        S.slin[c] = (uint32_t)elin(e);
+                        skey[c] = (unsigned long long)__double_as_longlong(ekey(e));
+                        slin[c] = (uint32_t)elin(e);
                     } else {
-                        S.skey[c] = ~0ull;
-                        S.slin[c] = ~0u;
+                        skey[c] = ~0ull;
+                        slin[c] = ~0u;
                     }
-                    S.sidx[c] = (uint16_t)c;
+                    sidx[c] = (uint16_t)c;
                 }
                 __syncthreads();
                 if (n <= NT) {
@@ -1084,29 +1093,29 @@ struct Query {
                     int rank = 0;
                     const int c = threadIdx.x;
                     if (c < n) {
-                        kc = S.skey[c];
-                        lc = S.slin[c];
+                        kc = skey[c];
+                        lc = slin[c];
                         for (int y = 0; y < n; y++) {
-                            const unsigned long long ky = S.skey[y];
-                            rank += (ky < kc || (ky == kc && S.slin[y] < lc)) ? 1 : 0;
+                            const unsigned long long ky = skey[y];
+                            rank += (ky < kc || (ky == kc && slin[y] < lc)) ? 1 : 0;
                         }
                     }
                     __syncthreads();
                     if (c < n) {
-                        S.skey[rank] = kc;
-                        S.slin[rank] = lc;
-                        S.sidx[rank] = (uint16_t)c;
+                        skey[rank] = kc;
+                        slin[rank] = lc;
+                        sidx[rank] = (uint16_t)c;
                     }
                     __syncthreads();
                 } else {
-                    bitonic_sort_cells(S, P2);
+                    bitonic_sort_cells(skey, slin, sidx, P2);
                 }
                 // first sorted position where the running count reaches need
                 if (threadIdx.x == 0) S.nlist = 0xFFFFFFFFu;
                 unsigned long long run = 0;
                 for (int base = 0; base < n; base += NT) {
                     int pidx = base + threadIdx.x;
-                    uint32_t g = pidx < n ? (uint32_t)cur[S.sidx[pidx]].y : 0u;
+                    uint32_t g = pidx < n ? (uint32_t)cur[sidx[pidx]].y : 0u;
                     uint32_t tot;
                     uint32_t ex = block_excl_scan(S, g, &tot);
                     if (pidx < n && run + ex < need && run + ex + g >= need) S.nlist = pidx;
@@ -1117,8 +1126,8 @@ struct Query {
                 __syncthreads();
                 int cut = (int)S.nlist;  // always found: total >= need
                 if (cut == -1) cut = n - 1;
-                if (threadIdx.x == 0) S.cut_key = S.skey[cut];
-                for (int c = threadIdx.x; c <= cut; c += NT) other[c] = cur[S.sidx[c]];
+                if (threadIdx.x == 0) S.cut_key = skey[cut];
+                for (int c = threadIdx.x; c <= cut; c += NT) other[c] = cur[sidx[c]];
                 __syncthreads();
                 emit(other, cut + 1, -1, 0);
                 return;
@@ -1326,16 +1335,16 @@ struct Query {
             __syncthreads();
             for (int x = threadIdx.x; x < T; x += NT) {
                 const unsigned long long key = ((unsigned long long)__float_as_uint(__ldg(u + x)) << 32) | (uint32_t)x;
-                if ((any || key > klast) && key <= kE) S.skey[atomicAdd(&S.tcnt, 1u)] = key;
+                if ((any || key > klast) && key <= kE) skey[atomicAdd(&S.tcnt, 1u)] = key;
             }
             __syncthreads();
             int P2 = 1;
             while (P2 < E) P2 <<= 1;
-            for (int i = E + threadIdx.x; i < P2; i += NT) S.skey[i] = ~0ull;
+            for (int i = E + threadIdx.x; i < P2; i += NT) skey[i] = ~0ull;
             __syncthreads();
-            bitonic_sort_u64(S.skey, P2);
+            bitonic_sort_u64(skey, P2);
             for (int i = threadIdx.x; i < E; i += NT) {
-                const unsigned long long kv = S.skey[i];
+                const unsigned long long kv = skey[i];
                 srw[tp + i] = __uint_as_float((uint32_t)(kv >> 32));
                 ow[tp + i] = (int32_t)(kv & 0xFFFFFFFFull);
             }
@@ -1788,15 +1797,15 @@ struct Query {
             }
             return;
         }
-        topk_compact(S, k);
+        topk_compact(S, tk, k);
         uint32_t n = S.ntk;
         int cnt = (int)min((unsigned long long)k, ncand);
         if (n <= 512) {
             // keys are unique: each key's rank is its output position
             for (int x = threadIdx.x; x < (int)n; x += NT) {
-                const unsigned long long kx = S.tk[x];
+                const unsigned long long kx = tk[x];
                 int rank = 0;
-                for (uint32_t y = 0; y < n; y++) rank += S.tk[y] < kx ? 1 : 0;
+                for (uint32_t y = 0; y < n; y++) rank += tk[y] < kx ? 1 : 0;
                 A.out_d[qo * k + rank] = __uint_as_float((uint32_t)(kx >> 32));
                 A.out_ids[qo * k + rank] = (uint32_t)kx;
             }
@@ -1804,11 +1813,11 @@ struct Query {
             int P2 = 1;
             while (P2 < (int)n) P2 <<= 1;
             for (int i = threadIdx.x; i < P2; i += NT)
-                if (i >= (int)n) S.tk[i] = ~0ull;
+                if (i >= (int)n) tk[i] = ~0ull;
             __syncthreads();
-            bitonic_sort_u64(S.tk, P2);
+            bitonic_sort_u64(tk, P2);
             for (int x = threadIdx.x; x < cnt; x += NT) {
-                unsigned long long kk = S.tk[x];
+                unsigned long long kk = tk[x];
                 A.out_d[qo * k + x] = __uint_as_float((uint32_t)(kk >> 32));
                 A.out_ids[qo * k + x] = (uint32_t)kk;
             }
@@ -1831,7 +1840,8 @@ __global__ void __launch_bounds__(NT, BPQ_MINB) search_kernel(Args<KT, OffT> A) 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem &S = *reinterpret_cast<Smem *>(smem_raw);
     float *tab = reinterpret_cast<float *>(smem_raw + sizeof(Smem));
-    float *lut = tab + (ENGINE == BPQ_ENGINE_FBPQ ? M * A.K : 0);
+    // per-cell LUT / cp.async stages (FBPQ) and the sort arrays share the region after the table
+    float *lut = tab + (ENGINE == BPQ_ENGINE_FBPQ ? M * A.K : ((A.D + 3) & ~3));
     KT *s1s = reinterpret_cast<KT *>(tab + A.tab_floats);
     KT *s2s = s1s + A.sr_smem;
 #ifdef BPQ_PHASE_PROF
@@ -1889,7 +1899,8 @@ __global__ void __launch_bounds__(NT, BPQ_MINB) search_kernel(Args<KT, OffT> A) 
             }
         }
         __syncthreads();
-        Query<ENGINE, MT, KT, OffT, SPARSE_ONLY> Q(A, S, qi, tab, lut, s1s, s2s);
+        Query<ENGINE, MT, KT, OffT, SPARSE_ONLY> Q(A, S, qi, tab, lut, s1s, s2s,
+                                                   reinterpret_cast<unsigned long long *>(smem_raw + A.tk_off));
         Q.run();
         Q.finish();
         __syncthreads();
@@ -1898,9 +1909,15 @@ __global__ void __launch_bounds__(NT, BPQ_MINB) search_kernel(Args<KT, OffT> A) 
 
 unsigned long long *g_prof_buffer = nullptr;
 
-size_t dyn_smem_bytes(int tab_floats, int sr_smem, size_t kt_size) {
-    return sizeof(Smem) + (size_t)tab_floats * 4 + 2 * (size_t)sr_smem * kt_size;
+// dynamic shared memory: Smem | per-query table | sorted-key prefixes | top-k buffer
+size_t tk_offset(int tab_floats, int sr_smem, size_t kt_size) {
+    return (sizeof(Smem) + (size_t)tab_floats * 4 + 2 * (size_t)sr_smem * kt_size + 15) & ~(size_t)15;
 }
+size_t dyn_smem_bytes(int tab_floats, int sr_smem, size_t kt_size, int tkcap) {
+    return tk_offset(tab_floats, sr_smem, kt_size) + (size_t)tkcap * 8;
+}
+// top-k buffer: k rounded up to 256 plus one round of offers (the largest round is NT * kUnroll)
+int topk_capacity(int k) { return ((k + 255) & ~255) + NT * kUnroll; }
 
 int g_num_sms = 0;
 
@@ -1938,12 +1955,15 @@ int launch_one(const Index &ix, const float *queries, int64_t q0, int64_t nq, in
     Args<float, uint32_t> A{};
     A.M = ix.M;
     // fold + per-cell LUT (exact FBPQ), or fold + the large-cell cp.async stages (point-term FBPQ)
-    A.tab_floats = ENGINE != BPQ_ENGINE_FBPQ ? ix.D
-                   : (MT != 0 && ix.pterm != nullptr) ? ix.M * ix.K + pipe_stage_bytes(ix.M) / 4
-                                                      : 2 * ix.M * ix.K;
+    // + the region shared by the LUT or cp.async stages and the sort arrays
+    A.tab_floats = ENGINE != BPQ_ENGINE_FBPQ ? ((ix.D + 3) & ~3) + kSortBytes / 4
+                   : (MT != 0 && ix.pterm != nullptr) ? ix.M * ix.K + std::max(pipe_stage_bytes(ix.M), kSortBytes) / 4
+                                                      : ix.M * ix.K + std::max(ix.M * ix.K * 4, kSortBytes) / 4;
     A.tab_floats = (A.tab_floats + 3) & ~3;
     A.sr_smem = 0;  // sorted keys are read through L1: only active lines are probed
-    const size_t smem = dyn_smem_bytes(A.tab_floats, A.sr_smem, sizeof(float));
+    A.tkcap = topk_capacity(k);
+    A.tk_off = (int)tk_offset(A.tab_floats, A.sr_smem, sizeof(float));
+    const size_t smem = dyn_smem_bytes(A.tab_floats, A.sr_smem, sizeof(float), A.tkcap);
     // first pass over a partially sorted sparse table: sparse traversal only
     const bool sparse_only = MT != 0 && ix.rowptr != nullptr && ws.topP < ix.T && ws.qlist == nullptr;
     int n_cta = 0;
