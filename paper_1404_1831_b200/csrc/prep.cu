@@ -231,8 +231,11 @@ __global__ void __launch_bounds__(kSortThreads) row_sort_kernel(
 constexpr int kCutMin = 256;
 constexpr int kBuckets = 1024;
 
-template <int ITEMS, int P>
-__global__ void __launch_bounds__(kSortThreads, ITEMS <= 8 ? 3 : 1) row_topk_kernel(
+// SMEM_KEYS (large T): each thread's keys live in dynamic shared memory at
+// the positions it loaded (no barrier needed, a thread only reads its own),
+// which frees the registers that capped these rows at one CTA per SM.
+template <int ITEMS, int P, bool SMEM_KEYS>
+__global__ void __launch_bounds__(kSortThreads, SMEM_KEYS ? 2 : (ITEMS <= 8 ? 3 : 1)) row_topk_kernel(
     const float *__restrict__ Q, int D, const float *__restrict__ dots1,
     const float *__restrict__ dots2, const float *__restrict__ cn1,
     const float *__restrict__ cn2, int T, float *__restrict__ sr1, float *__restrict__ sr2,
@@ -277,7 +280,12 @@ __global__ void __launch_bounds__(kSortThreads, ITEMS <= 8 ? 3 : 1) row_topk_ker
     // striped float4 arrangement (coalesced 16-byte loads/stores); the
     // order of keys across threads is irrelevant to the (value, index) sort
     auto ix = [](int s) { return ((s >> 2) * kSortThreads + (int)threadIdx.x) * 4 + (s & 3); };
-    unsigned int keys[ITEMS];
+    unsigned int kreg[SMEM_KEYS ? 1 : ITEMS];
+    extern __shared__ unsigned int skeys[];
+    auto KEY = [&](int s) -> unsigned int & {
+        if constexpr (SMEM_KEYS) return skeys[ix(s)];
+        else return kreg[s];
+    };
     unsigned int kmin = 0xFFFFFFFFu, kmax = 0u;
     auto rval = [&](float c, float d) {
         float r = __fadd_rn(__fsub_rn(c, __fmul_rn(2.f, d)), qn);
@@ -292,18 +300,18 @@ __global__ void __launch_bounds__(kSortThreads, ITEMS <= 8 ? 3 : 1) row_topk_ker
                 const float4 cv = __ldg(reinterpret_cast<const float4 *>(cn + b));
                 const float4 rv = make_float4(rval(cv.x, dv.x), rval(cv.y, dv.y), rval(cv.z, dv.z), rval(cv.w, dv.w));
                 *reinterpret_cast<float4 *>(ru + b) = rv;
-                keys[j * 4 + 0] = __float_as_uint(rv.x);
-                keys[j * 4 + 1] = __float_as_uint(rv.y);
-                keys[j * 4 + 2] = __float_as_uint(rv.z);
-                keys[j * 4 + 3] = __float_as_uint(rv.w);
+                KEY(j * 4 + 0) = __float_as_uint(rv.x);
+                KEY(j * 4 + 1) = __float_as_uint(rv.y);
+                KEY(j * 4 + 2) = __float_as_uint(rv.z);
+                KEY(j * 4 + 3) = __float_as_uint(rv.w);
 #pragma unroll
                 for (int e = 0; e < 4; e++) {
-                    kmin = min(kmin, keys[j * 4 + e]);
-                    kmax = max(kmax, keys[j * 4 + e]);
+                    kmin = min(kmin, KEY(j * 4 + e));
+                    kmax = max(kmax, KEY(j * 4 + e));
                 }
             } else {
 #pragma unroll
-                for (int e = 0; e < 4; e++) keys[j * 4 + e] = 0xFFFFFFFFu;
+                for (int e = 0; e < 4; e++) KEY(j * 4 + e) = 0xFFFFFFFFu;
             }
         }
     } else {
@@ -312,12 +320,12 @@ __global__ void __launch_bounds__(kSortThreads, ITEMS <= 8 ? 3 : 1) row_topk_ker
             const int idx = ix(s);
             if (idx < T) {
                 const float r = rval(__ldg(cn + idx), __ldg(dots + idx));
-                keys[s] = __float_as_uint(r);
+                KEY(s) = __float_as_uint(r);
                 ru[idx] = r;
-                kmin = min(kmin, keys[s]);
-                kmax = max(kmax, keys[s]);
+                kmin = min(kmin, KEY(s));
+                kmax = max(kmax, KEY(s));
             } else {
-                keys[s] = 0xFFFFFFFFu;
+                KEY(s) = 0xFFFFFFFFu;
             }
         }
     }
@@ -354,8 +362,8 @@ __global__ void __launch_bounds__(kSortThreads, ITEMS <= 8 ? 3 : 1) row_topk_ker
         __syncthreads();
 #pragma unroll
         for (int s = 0; s < ITEMS; s++) {
-            if (ix(s) < T && keys[s] >= lo) {
-                const unsigned int bkt = (keys[s] - lo) >> shift;
+            if (ix(s) < T && KEY(s) >= lo) {
+                const unsigned int bkt = (KEY(s) - lo) >> shift;
                 if (bkt < (unsigned int)kBuckets) atomicAdd(&hist[bkt], 1u);
             }
         }
@@ -416,7 +424,7 @@ __global__ void __launch_bounds__(kSortThreads, ITEMS <= 8 ? 3 : 1) row_topk_ker
     __syncthreads();
 #pragma unroll
     for (int s = 0; s < ITEMS; s++)
-        if (ix(s) < T && keys[s] < cut) atomicAdd(&hist[(keys[s] - gmin) >> sshift], 1u);
+        if (ix(s) < T && KEY(s) < cut) atomicAdd(&hist[(KEY(s) - gmin) >> sshift], 1u);
     __syncthreads();
     unsigned int total;
     {
@@ -438,9 +446,9 @@ __global__ void __launch_bounds__(kSortThreads, ITEMS <= 8 ? 3 : 1) row_topk_ker
     for (int w = 0; w < kSortThreads / 32; w++) maxb = max(maxb, s_wsum[w]);
 #pragma unroll
     for (int s = 0; s < ITEMS; s++) {
-        if (ix(s) < T && keys[s] < cut) {
-            const unsigned int at = atomicAdd(&hist[(keys[s] - gmin) >> sshift], 1u);
-            sk64[at] = ((unsigned long long)keys[s] << 32) | (unsigned int)ix(s);
+        if (ix(s) < T && KEY(s) < cut) {
+            const unsigned int at = atomicAdd(&hist[(KEY(s) - gmin) >> sshift], 1u);
+            sk64[at] = ((unsigned long long)KEY(s) << 32) | (unsigned int)ix(s);
         }
     }
     __syncthreads();
@@ -498,8 +506,18 @@ int launch_row_topk_t(const float *Q, int64_t nq, int32_t D, const float *dots1,
                       const float *cn1, const float *cn2, int32_t T, float *sr1, float *sr2, int32_t *ord1,
                       int32_t *ord2, float *ru1, float *ru2, int32_t *plen, cudaStream_t stream) {
     dim3 grid((unsigned)nq, 2);
-    row_topk_kernel<ITEMS, kTopP><<<grid, kSortThreads, 0, stream>>>(Q, D, dots1, dots2, cn1, cn2, T, sr1, sr2,
-                                                                   ord1, ord2, ru1, ru2, plen);
+    constexpr bool kSmem = ITEMS > 8;
+    const size_t smem = kSmem ? (size_t)ITEMS * kSortThreads * 4 : 0;
+    if (kSmem) {
+        static bool configured = false;
+        if (!configured) {
+            BPQ_CUDA_TRY(cudaFuncSetAttribute(row_topk_kernel<ITEMS, kTopP, kSmem>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            configured = true;
+        }
+    }
+    row_topk_kernel<ITEMS, kTopP, kSmem><<<grid, kSortThreads, smem, stream>>>(Q, D, dots1, dots2, cn1, cn2, T, sr1,
+                                                                            sr2, ord1, ord2, ru1, ru2, plen);
     BPQ_CUDA_TRY(cudaGetLastError());
     return BPQ_OK;
 }

@@ -253,6 +253,33 @@ def test_partial_sort_and_retry_pass(torch_cuda, oracle):
         check_topk(d[:16], i[:16], c[:16], wd, wi, wc, _qn(q[:16]), min_exact_frac=0.85)
 
 
+@pytest.mark.parametrize("t", [4500, 8200])
+def test_partial_sort_large_t_matches_full_sort(torch_cuda, t):
+    """Row top-k with the keys in shared memory (T > 4096: 16 and 32 keys per
+    thread) must give the same results as the full-sort path."""
+    import torch
+
+    from paper_1404_1831_b200 import encode
+
+    rng = np.random.default_rng(t)
+    dim, m, kk, n = 16, 4, 16, 60_000
+    cent = rng.normal(scale=6.0, size=(300, dim)).astype(np.float32)
+    base = (cent[rng.integers(0, 300, n)] + rng.normal(size=(n, dim))).astype(np.float32)
+    c1 = (base[rng.integers(0, n, t), : dim // 2] + rng.normal(scale=0.5, size=(t, dim // 2))).astype(np.float32)
+    c2 = (base[rng.integers(0, n, t), dim // 2 :] + rng.normal(scale=0.5, size=(t, dim // 2))).astype(np.float32)
+    books = rng.normal(scale=0.4, size=(m, kk, dim // m)).astype(np.float32)
+    dix = encode.build_index(base, c1, c2, books)
+    assert dix.row_ptr is not None
+    q = (cent[rng.integers(0, 300, 64)] + rng.normal(size=(64, dim))).astype(np.float32)
+    for L, k in ((100, 10), (5000, 50)):
+        part = dix.search(q, L, k, "fbpq", ncand=True)
+        popped = torch.empty(q.shape[0], dtype=torch.int64, device="cuda")
+        full = dix.search(q, L, k, "fbpq", ncand=True, popped=popped)   # popped forces the full sort
+        for x, y in zip(part.numpy(), full.numpy()):
+            np.testing.assert_array_equal(x, y)
+        np.testing.assert_array_equal(part.ncand.cpu().numpy(), full.ncand.cpu().numpy())
+
+
 def test_empty_index_returns_nothing(torch_cuda):
     from paper_1404_1831_b200 import DeviceIndex
 
