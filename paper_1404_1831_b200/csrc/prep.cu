@@ -108,9 +108,12 @@ __global__ void __launch_bounds__(256) coarse_dots_kernel(const float *__restric
 
 // FBPQ query tables for a batch (fbpq.py:140-144): for every query, part p
 // and codeword c, fold[q][p][c] = fine_norms[p][c] - 2 * (books[p][c] . q_p).
-// One CTA per (32-query tile, part): the part's codebook (K x ds) and the
-// query slices are staged in shared memory; thread c owns codeword c.
-constexpr int FQ = 32;
+// One CTA per (64-query tile, part): the part's codebook (K x ds, padded to
+// ds + 1 so the strided codeword reads are conflict-free) and the query
+// slices are staged in shared memory.  Each thread owns 4 codewords (c = cg +
+// 64 i) x 16 queries in registers; every dot is the same ascending-u fmaf
+// chain from 0 as a scalar loop, so the values do not depend on the tiling.
+constexpr int FQ = 64;
 
 __global__ void __launch_bounds__(256) fold_kernel(const float *__restrict__ Q, int64_t nq, int D, int M,
                                                    int K, const float *__restrict__ books,
@@ -120,7 +123,7 @@ __global__ void __launch_bounds__(256) fold_kernel(const float *__restrict__ Q, 
     const int p = blockIdx.y;
     const int ds = D / M;
     const int64_t q0 = (int64_t)blockIdx.x * FQ;
-    float *bk = fs;              // [K][ds+1] (padded: conflict-free column reads)
+    float *bk = fs;                 // [K][ds+1]
     float *qs = fs + K * (ds + 1);  // [FQ][ds]
     for (int x = threadIdx.x; x < K * ds; x += blockDim.x) {
         const int c = x / ds, u = x - c * ds;
@@ -132,16 +135,35 @@ __global__ void __launch_bounds__(256) fold_kernel(const float *__restrict__ Q, 
         qs[x] = q < nq ? __ldg(Q + q * D + p * ds + u) : 0.f;
     }
     __syncthreads();
-    for (int c = threadIdx.x; c < K; c += blockDim.x) {
+    const int cg = threadIdx.x & 63, qg = threadIdx.x >> 6;
+    float acc[4][16];
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+#pragma unroll
+        for (int j = 0; j < 16; j++) acc[i][j] = 0.f;
+    for (int u = 0; u < ds; u++) {
+        float b[4];
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            const int c = cg + 64 * i;
+            b[i] = c < K ? bk[c * (ds + 1) + u] : 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+            const float qv = qs[(qg * 16 + j) * ds + u];
+#pragma unroll
+            for (int i = 0; i < 4; i++) acc[i][j] = fmaf(b[i], qv, acc[i][j]);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        const int c = cg + 64 * i;
+        if (c >= K) continue;
         const float fn = __ldg(fine_norms + p * K + c);
-        const float *b = bk + c * (ds + 1);
-        for (int qq = 0; qq < FQ; qq++) {
-            const int64_t q = q0 + qq;
-            if (q >= nq) break;
-            const float *qv = qs + qq * ds;
-            float dot = 0.f;
-            for (int u = 0; u < ds; u++) dot = fmaf(b[u], qv[u], dot);
-            fold[(q * M + p) * K + c] = __fsub_rn(fn, __fmul_rn(2.f, dot));
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+            const int64_t q = q0 + qg * 16 + j;
+            if (q < nq) fold[(q * M + p) * K + c] = __fsub_rn(fn, __fmul_rn(2.f, acc[i][j]));
         }
     }
 }

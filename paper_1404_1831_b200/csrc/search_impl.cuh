@@ -61,7 +61,7 @@ constexpr int kEnumBatch = 8;             // cell-table reads in flight per thre
 #define BPQ_PIPE_U 2
 #endif
 #ifndef BPQ_PIPE_S
-#define BPQ_PIPE_S 2
+#define BPQ_PIPE_S 3
 #endif
 constexpr int kPipeU = BPQ_PIPE_U;        // large-cell scan: entries per thread per round
 constexpr int kPipeR = NT * kPipeU;       // entries per round
