@@ -257,7 +257,7 @@ constexpr int kBuckets = 1024;
 // the positions it loaded (no barrier needed, a thread only reads its own),
 // which frees the registers that capped these rows at one CTA per SM.
 template <int ITEMS, int P, bool SMEM_KEYS>
-__global__ void __launch_bounds__(kSortThreads, SMEM_KEYS ? 2 : (ITEMS <= 8 ? 3 : 1)) row_topk_kernel(
+__global__ void __launch_bounds__(kSortThreads, SMEM_KEYS ? 2 : (ITEMS <= 8 ? 4 : 1)) row_topk_kernel(
     const float *__restrict__ Q, int D, const float *__restrict__ dots1,
     const float *__restrict__ dots2, const float *__restrict__ cn1,
     const float *__restrict__ cn2, int T, float *__restrict__ sr1, float *__restrict__ sr2,
