@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(256) coarse_dots_kernel(const float *__restric
 // chain from 0 as a scalar loop, so the values do not depend on the tiling.
 constexpr int FQ = 64;
 
-__global__ void __launch_bounds__(256) fold_kernel(const float *__restrict__ Q, int64_t nq, int D, int M,
+__global__ void __launch_bounds__(256, 3) fold_kernel(const float *__restrict__ Q, int64_t nq, int D, int M,
                                                    int K, const float *__restrict__ books,
                                                    const float *__restrict__ fine_norms,
                                                    float *__restrict__ fold) {
