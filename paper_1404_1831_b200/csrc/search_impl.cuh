@@ -792,6 +792,80 @@ struct Query {
         PROF(pv);
     }
 
+    // Multi-D-ADC / HBPQ, one large cell: the cell's residual lookup table
+    // LUT[p][c] = sum_u ((q_h[u] - c_h[row][u]) - book[c][u])^2 with the
+    // global books (Multi-D-ADC) or the row's / column's local books (HBPQ,
+    // the per-cell tables of BASELINE configs[2]), each part summed in the
+    // reference's order (numba_backend.py:165-176, 198-210); an entry then
+    // costs M shared-memory lookups.  Each half is rebuilt only when the
+    // cell's row (column) codeword changes.  The per-part split regroups the
+    // reference's single running sum (within 1e-6 relative).
+    __device__ void scan_cell_recon_lut(int oi, int oj, uint32_t lst, uint32_t lc) {
+        const int pv = PROF(PH_LUT);
+        (void)pv;
+        const int M2 = M / 2, K = A.K, ds = A.ds, dh = A.dh;
+        const int lo_idx = oi == lut_i ? M2 * K : 0;
+        const int hi_idx = oj == lut_j ? M2 * K : M * K;
+        if (lo_idx < hi_idx) {
+            for (int idx = lo_idx + threadIdx.x; idx < hi_idx; idx += NT) {
+                const int p = idx / K, c = idx - p * K;
+                const int hp = p < M2 ? p : p - M2;
+                const int row = p < M2 ? oi : oj;
+                const float *cr = (p < M2 ? A.c1 : A.c2) + (size_t)row * dh + hp * ds;
+                const float *qv = tab + (p < M2 ? 0 : dh) + hp * ds;
+                const float *bk;
+                if constexpr (ENGINE == BPQ_ENGINE_HBPQ)
+                    bk = (p < M2 ? A.bank1 : A.bank2) + (((size_t)row * M2 + hp) * K + c) * ds;
+                else
+                    bk = A.books + ((size_t)p * K + c) * ds;
+                float acc = 0.f;
+                if ((ds & 3) == 0) {
+                    for (int u = 0; u < ds; u += 4) {
+                        const float4 cv = __ldg(reinterpret_cast<const float4 *>(cr + u));
+                        const float4 bv = __ldg(reinterpret_cast<const float4 *>(bk + u));
+                        const float ce[4] = {cv.x, cv.y, cv.z, cv.w};
+                        const float be[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+                        for (int z = 0; z < 4; z++) {
+                            const float d = __fsub_rn(__fsub_rn(qv[u + z], ce[z]), be[z]);
+                            acc = __fadd_rn(acc, __fmul_rn(d, d));
+                        }
+                    }
+                } else {
+                    for (int u = 0; u < ds; u++) {
+                        const float d = __fsub_rn(__fsub_rn(qv[u], __ldg(cr + u)), __ldg(bk + u));
+                        acc = __fadd_rn(acc, __fmul_rn(d, d));
+                    }
+                }
+                lut[idx] = acc;
+            }
+            __syncthreads();
+        }
+        lut_i = oi;
+        lut_j = oj;
+        for (uint32_t e0 = 0; e0 < lc; e0 += NT * kLutUnroll) {
+            uint32_t w[kLutUnroll][4];
+#pragma unroll
+            for (int u = 0; u < kLutUnroll; u++) {
+                const uint32_t e = e0 + u * NT + threadIdx.x;
+                if (e < lc) load_code<MT>(A.codes + (size_t)(lst + e) * M, w[u], M);
+            }
+#pragma unroll
+            for (int u = 0; u < kLutUnroll; u++) {
+                const uint32_t e = e0 + u * NT + threadIdx.x;
+                if (e < lc) {
+                    float acc = 0.f;
+#pragma unroll
+                    for (int p = 0; p < M; p++) acc = __fadd_rn(acc, lut[p * K + code_at(w[u], p)]);
+                    offer_lazy(acc, A.ids + lst + e);
+                }
+            }
+            round_end(NT * kLutUnroll);
+        }
+        __syncthreads();
+        PROF(pv);
+    }
+
     // Visit a list of cells: scan their entries (search) or record them
     // (traversal stage).  filt_d < 0: all cells; else only cells whose digit
     // filt_d is < filt_v.
@@ -826,6 +900,8 @@ struct Query {
                         float t0 = __fsub_rn(S.qnorm, __fmul_rn(2.f, s));
                         cb = __fadd_rn(__fadd_rn(t0, __ldg(A.cn1 + oi)), __ldg(A.cn2 + oj));
                         big = lc >= (uint32_t)A.lut_min;
+                    } else if constexpr (ENGINE == BPQ_ENGINE_BASELINE || ENGINE == BPQ_ENGINE_HBPQ) {
+                        big = MT != 0 && erot == nullptr && lc >= (uint32_t)A.lut_min;
                     }
                 }
             }
@@ -912,6 +988,13 @@ struct Query {
                             ncand += S.ccnt[t];
                             scan_cell_lut(S.coi[t], S.coj[t], S.cstart[t], S.ccnt[t], S.cbase[t]);
                         }
+                    }
+                } else if constexpr ((ENGINE == BPQ_ENGINE_BASELINE || ENGINE == BPQ_ENGINE_HBPQ) && MT != 0) {
+                    const uint32_t nb = S.nbig;
+                    for (uint32_t x = 0; x < nb; x++) {
+                        const int t = S.bigs[x];
+                        ncand += S.ccnt[t];
+                        scan_cell_recon_lut(S.coi[t], S.coj[t], S.cstart[t], S.ccnt[t]);
                     }
                 } else if constexpr (ENGINE == BPQ_ENGINE_FBPQ) {
                     const uint32_t nb = S.nbig;
@@ -1070,6 +1153,7 @@ struct Query {
     // exact cutoff inside the final band (weighted select, then smem sort)
     __device__ void final_select(int4 *cur, int4 *other, int n, unsigned long long need) {
         PROF(PH_FINAL);
+        lut_i = lut_j = -1;  // the sort arrays below alias the per-cell LUT
         for (int d = 0;; d++) {
             if (n <= kSortCap) {
                 int P2 = 1;
@@ -1129,6 +1213,7 @@ struct Query {
                 if (threadIdx.x == 0) S.cut_key = skey[cut];
                 for (int c = threadIdx.x; c <= cut; c += NT) other[c] = cur[sidx[c]];
                 __syncthreads();
+                lut_i = lut_j = -1;  // the sort overwrote the aliased LUT
                 emit(other, cut + 1, -1, 0);
                 return;
             }
@@ -1292,6 +1377,7 @@ struct Query {
     // shared memory and appended to sr/ord.  Only queries whose traversal
     // outgrows the partial sort pay for it.
     __device__ void extend(int h, int need) {
+        lut_i = lut_j = -1;  // the sort arrays below alias the per-cell LUT
         int tp = h ? tp2 : tp1;
         const float *u = h ? u2 : u1;
         float *srw = const_cast<float *>(reinterpret_cast<const float *>(h ? sr2 : sr1));
@@ -1956,7 +2042,7 @@ int launch_one(const Index &ix, const float *queries, int64_t q0, int64_t nq, in
     A.M = ix.M;
     // fold + per-cell LUT (exact FBPQ), or fold + the large-cell cp.async stages (point-term FBPQ)
     // + the region shared by the LUT or cp.async stages and the sort arrays
-    A.tab_floats = ENGINE != BPQ_ENGINE_FBPQ ? ((ix.D + 3) & ~3) + kSortBytes / 4
+    A.tab_floats = ENGINE != BPQ_ENGINE_FBPQ ? ((ix.D + 3) & ~3) + std::max(ix.M * ix.K * 4, kSortBytes) / 4
                    : (MT != 0 && ix.pterm != nullptr) ? ix.M * ix.K + std::max(pipe_stage_bytes(ix.M), kSortBytes) / 4
                                                       : ix.M * ix.K + std::max(ix.M * ix.K * 4, kSortBytes) / 4;
     A.tab_floats = (A.tab_floats + 3) & ~3;

@@ -280,6 +280,37 @@ def test_partial_sort_large_t_matches_full_sort(torch_cuda, t):
         np.testing.assert_array_equal(part.ncand.cpu().numpy(), full.ncand.cpu().numpy())
 
 
+@pytest.mark.parametrize("m", [8, 16])
+def test_large_cells_every_engine_vs_oracle(torch_cuda, oracle, m):
+    """Few coarse codewords, so cells hold hundreds of entries and take the
+    per-cell paths: FBPQ point term (cp.async stages) and exact LUT, and the
+    Multi-D-ADC / HBPQ residual lookup tables.  Contract of SURVEY §8c(ii)."""
+    from paper_1404_1831_b200 import DeviceIndex
+
+    rng = np.random.default_rng(77 + m)
+    t, dim, kk, n = 10, 32, 32, 60_000
+    base = rng.normal(size=(n, dim)).astype(np.float32)
+    c1 = base[rng.choice(n, t, replace=False), : dim // 2].copy()
+    c2 = base[rng.choice(n, t, replace=False), dim // 2 :].copy()
+    books = (0.3 * rng.normal(size=(m, kk, dim // m))).astype(np.float32)
+    off, ids, codes = oracle.build_index(base, c1, c2, books)
+    assert np.diff(off).max() >= 1000
+    bank1 = (0.3 * rng.normal(size=(t, m // 2, kk, dim // m))).astype(np.float32)
+    bank2 = (0.3 * rng.normal(size=(t, m // 2, kk, dim // m))).astype(np.float32)
+    idx = oracle.Index(c1, c2, off, ids, codes, books=books)
+    hidx = oracle.Index(c1, c2, off, ids, codes, bank1=bank1, bank2=bank2)
+    q = rng.normal(size=(32, dim)).astype(np.float32)
+    dix = DeviceIndex(c1=c1, c2=c2, offsets=off, ids=ids, codes=codes, books=books, tables=idx.tables)
+    dex = DeviceIndex(c1=c1, c2=c2, offsets=off, ids=ids, codes=codes, books=books, tables=idx.tables,
+                      fbpq_exact=True)
+    hix = DeviceIndex(c1=c1, c2=c2, offsets=off, ids=ids, codes=codes, bank1=bank1, bank2=bank2)
+    for L, k in ((2000, 20), (20_000, 100)):
+        for eng, di, oi in (("fbpq", dix, idx), ("fbpq", dex, idx), ("baseline", dix, idx), ("hbpq", hix, hidx)):
+            wd, wi, wc, _ = oracle.search_batch_numpy(oi, eng, q, L, k)
+            d, i, c = di.search(q, L, k, eng).numpy()
+            check_topk(d, i, c, wd, wi, wc, _qn(q), min_exact_frac=0.9)
+
+
 def test_empty_index_returns_nothing(torch_cuda):
     from paper_1404_1831_b200 import DeviceIndex
 
