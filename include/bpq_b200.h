@@ -92,7 +92,11 @@ typedef struct bpq_index_desc {
      * gathers, within 1e-6 relative of the reference.  1: the reference's
      * exact operation order (numba_backend.py:231-242), bit-identical per
      * candidate given the same query tables.  The stage kernel
-     * bpq_scan_tables is always exact. */
+     * bpq_scan_tables is always exact.  The flag also governs Multi-D-ADC
+     * and HBPQ: 0 scores cells whose GLOBAL entry count is >= 256 through a
+     * per-cell residual table (per-part sums, within 1e-6 relative); 1 keeps
+     * the reference's single running sum (numba_backend.py:165-176,
+     * 198-210) for every candidate. */
     int32_t fbpq_exact;
 } bpq_index_desc;
 

@@ -51,6 +51,7 @@ struct Index {
     const float *books, *fine_norms, *cross1, *cross2, *bank1, *bank2;
     const float *rot, *rot1, *rot2;  // optional rotations (see bpq_index_desc)
     const float *pterm;  // FBPQ per-entry cross term [N] (null: exact reference-order scan)
+    bool exact;          // bpq_index_desc.fbpq_exact: reference operation order, all engines
     // populated-cell lists (optional): row i -> columns j, column j -> rows i
     const uint32_t *rowptr, *colptr;
     const uint16_t *rowcols, *colrows;

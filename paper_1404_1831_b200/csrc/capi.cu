@@ -172,7 +172,9 @@ extern "C" int bpq_index_create(const bpq_index_desc *d, int copy_from_host, bpq
         ix.rowptr = ix.colptr = nullptr;
         ix.rowcols = ix.colrows = nullptr;
         if (d->row_ptr && d->col_ptr && d->row_cols && d->col_rows) {
-            const size_t P = std::min<size_t>(N > 0 ? N : 1, T * T);
+            // the lists describe the traversal table (global_offsets when
+            // sharded): size them by its populated count, row_ptr[T]
+            const size_t P = std::max<size_t>(d->row_ptr[T], 1);
             rc |= copy_in(d->row_ptr, T + 1, ix.owned, &ix.rowptr);
             rc |= copy_in(d->col_ptr, T + 1, ix.owned, &ix.colptr);
             rc |= copy_in(d->row_cols, P, ix.owned, &ix.rowcols);
@@ -185,6 +187,7 @@ extern "C" int bpq_index_create(const bpq_index_desc *d, int copy_from_host, bpq
         }
     }
     ix.pterm = nullptr;
+    ix.exact = d->fbpq_exact != 0;
     if (ix.cross1 && ix.cross2 && ix.codes && N > 0 && !d->fbpq_exact) {
         float *pt = nullptr;
         if (cudaMalloc(&pt, N * sizeof(float)) != cudaSuccess) {
@@ -193,7 +196,12 @@ extern "C" int bpq_index_create(const bpq_index_desc *d, int copy_from_host, bpq
             return fail(BPQ_ERR_CUDA, "cannot allocate the FBPQ point-term array");
         }
         ix.owned.push_back(pt);
-        int rc = launch_point_term(ix.loff, ix.T, ix.M, ix.K, ix.codes, ix.cross1, ix.cross2, pt, 0);
+        // device mode borrows caller buffers that may still be in flight on
+        // any (possibly non-blocking) stream: drain the device first
+        int rc = cudaDeviceSynchronize() == cudaSuccess
+                     ? BPQ_OK
+                     : fail(BPQ_ERR_CUDA, cudaGetErrorString(cudaGetLastError()));
+        if (rc == BPQ_OK) rc = launch_point_term(ix.loff, ix.T, ix.M, ix.K, ix.codes, ix.cross1, ix.cross2, pt, 0);
         if (rc == BPQ_OK && cudaDeviceSynchronize() != cudaSuccess)
             rc = fail(BPQ_ERR_CUDA, cudaGetErrorString(cudaGetLastError()));
         if (rc) {

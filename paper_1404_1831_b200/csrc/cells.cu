@@ -60,7 +60,9 @@ size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 // query independent, so the batched scan reads 4 B per entry instead of
 // gathering M cross-table values (numba_backend.py:236-240 does the gathers
 // per query).  Summed in f64 and rounded once.  One CTA per cell row i with
-// cross1[i] staged in shared memory; entries of row i are contiguous.
+// cross1[i] staged in shared memory; the row's entries are contiguous and
+// are spread over the CTA (a billion-point row holds ~60K entries), each
+// thread finding its entry's column by binary search in the row's offsets.
 __global__ void point_term_kernel(const uint32_t *__restrict__ off, int t, int m, int k,
                                   const uint8_t *__restrict__ codes, const float *__restrict__ cross1,
                                   const float *__restrict__ cross2, float *__restrict__ pt) {
@@ -70,16 +72,19 @@ __global__ void point_term_kernel(const uint32_t *__restrict__ off, int t, int m
     for (int x = threadIdx.x; x < m2 * k; x += CT) c1s[x] = cross1[(size_t)i * m2 * k + x];
     __syncthreads();
     const uint32_t *row = off + (size_t)i * t;
-    for (int j = threadIdx.x; j < t; j += CT) {
-        const uint32_t g0 = row[j], g1 = row[j + 1];
-        const float *c2 = cross2 + (size_t)j * m2 * k;
-        for (uint32_t e = g0; e < g1; e++) {
-            const uint8_t *c = codes + (size_t)e * m;
-            double acc = 0.0;
-            for (int p = 0; p < m2; p++) acc += 2.0 * (double)c1s[p * k + c[p]];
-            for (int p = 0; p < m2; p++) acc += 2.0 * (double)__ldg(c2 + p * k + c[m2 + p]);
-            pt[e] = (float)acc;
+    const uint32_t e0 = row[0], e1 = row[t];
+    for (uint32_t e = e0 + threadIdx.x; e < e1; e += CT) {
+        int lo = 0, hi = t - 1;  // largest j with row[j] <= e (then row[j+1] > e)
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (__ldg(row + mid) <= e) lo = mid; else hi = mid - 1;
         }
+        const float *c2 = cross2 + (size_t)lo * m2 * k;
+        const uint8_t *c = codes + (size_t)e * m;
+        double acc = 0.0;
+        for (int p = 0; p < m2; p++) acc += 2.0 * (double)c1s[p * k + c[p]];
+        for (int p = 0; p < m2; p++) acc += 2.0 * (double)__ldg(c2 + p * k + c[m2 + p]);
+        pt[e] = (float)acc;
     }
 }
 

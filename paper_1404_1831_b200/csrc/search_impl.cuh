@@ -154,6 +154,7 @@ struct Args {
     const float *books, *fine_norms, *cross1, *cross2, *bank1, *bank2;
     const float *pterm;        // FBPQ per-entry point term (null: exact reference order)
     const float *rot1, *rot2;  // HBPQ per-half rotations (optional)
+    bool exact;                // reference operation order for every engine (bpq_index_desc.fbpq_exact)
     double rho;
     unsigned long long n_global;
     const float *queries;
@@ -901,7 +902,10 @@ struct Query {
                         cb = __fadd_rn(__fadd_rn(t0, __ldg(A.cn1 + oi)), __ldg(A.cn2 + oj));
                         big = lc >= (uint32_t)A.lut_min;
                     } else if constexpr (ENGINE == BPQ_ENGINE_BASELINE || ENGINE == BPQ_ENGINE_HBPQ) {
-                        big = MT != 0 && erot == nullptr && lc >= (uint32_t)A.lut_min;
+                        // decided on the GLOBAL cell count (e.y), so a cell takes the same
+                        // path on one GPU and on every shard; exact mode keeps the
+                        // reference's single running sum (no per-part regrouping)
+                        big = MT != 0 && erot == nullptr && !A.exact && (uint32_t)e.y >= (uint32_t)A.lut_min;
                     }
                 }
             }
@@ -2069,6 +2073,7 @@ int launch_one(const Index &ix, const float *queries, int64_t q0, int64_t nq, in
     A.loff = ix.loff;
     A.goff = ix.goff;
     A.sharded = ix.goff != ix.loff;
+    A.exact = ix.exact;
     A.ids = ix.ids;
     A.codes = ix.codes;
     A.books = ix.books;

@@ -108,14 +108,18 @@ class DeviceIndex:
 
     def __init__(self, *, c1, c2, offsets, ids, codes, books=None, tables=None, bank1=None,
                  bank2=None, global_offsets=None, device=None, num_entries_global=None, cell_lists="auto",
-                 rotation=None, rot1=None, rot2=None, fbpq_exact=None):
-        """``fbpq_exact``: score FBPQ candidates in the reference's exact
-        operation order (numba_backend.py:231-242) instead of through the
-        precomputed per-entry point term (bpq_index_desc.fbpq_exact); default
-        from the environment variable BPQ_FBPQ_EXACT=1."""
+                 rotation=None, rot1=None, rot2=None, fbpq_exact=None, exact=None):
+        """``fbpq_exact`` (alias ``exact``): score every candidate in the
+        reference's exact operation order -- FBPQ without the precomputed
+        per-entry point term (numba_backend.py:231-242), Multi-D-ADC / HBPQ
+        without the per-cell residual tables (numba_backend.py:165-176,
+        198-210); bpq_index_desc.fbpq_exact.  Default from the environment
+        variable BPQ_FBPQ_EXACT=1."""
         import torch
 
         self.device = torch.device(device if device is not None else "cuda")
+        if exact is not None:
+            fbpq_exact = exact
         if fbpq_exact is None:
             fbpq_exact = os.environ.get("BPQ_FBPQ_EXACT") == "1"
         self.fbpq_exact = bool(fbpq_exact)
@@ -191,7 +195,7 @@ class DeviceIndex:
                 raise ValueError("per-half rotation dimension must equal dim/2")
         self._build_cell_lists(cell_lists)
         self._handle = None
-        self._ws = None
+        self._ws = {}
         self._create()
 
     # ------------------------------------------------------ populated cells
@@ -292,6 +296,13 @@ class DeviceIndex:
         on ``stream`` (default: torch's current stream), no host sync."""
         import torch
 
+        if stream is not None and stream != torch.cuda.current_stream(self.device):
+            # upload, output/workspace allocation and the kernels all on the
+            # caller's stream, so nothing is read before it is written and the
+            # caching allocator ties every temporary to that stream
+            with torch.cuda.stream(stream):
+                return self.search(queries, L, k, engine, out=out, workspace=workspace, stream=None,
+                                   ncand=ncand, popped=popped, stage_events=stage_events)
         if engine not in _lib.ENGINES:
             raise ValueError(f"unknown engine {engine!r}")
         if engine == "hbpq" and self.kind != "hbpq":
@@ -319,9 +330,13 @@ class DeviceIndex:
             )
         need = self.workspace_bytes(engine, nq, L, k)
         if workspace is None:
-            if self._ws is None or self._ws.numel() < need:
-                self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
-            workspace = self._ws
+            # one cached workspace per stream: concurrent searches on
+            # different streams never share scratch
+            key = torch.cuda.current_stream(self.device).cuda_stream
+            ws = self._ws.get(key)
+            if ws is None or ws.numel() < need:
+                ws = self._ws[key] = torch.empty(need, dtype=torch.uint8, device=self.device)
+            workspace = ws
         elif workspace.numel() < need:
             raise ValueError(f"workspace too small: {workspace.numel()} < {need}")
         lib = _lib.load()
