@@ -46,10 +46,12 @@ def log(*a):
 
 # --------------------------------------------------------------------- setup
 CONFIGS = {
+    # c1/c2: codebooks trained by the reference itself (tests/golden/c1_books.npz), base and queries from
+    # the blocked numpy stream that bench_reference.py (the --impl reference arm) draws identically
     "c1": dict(n=10_000_000, dim=128, ncomp=4096, t=4096, m=8, k=256, nq=10_000, L=10_000, topk=100,
-               engine="fbpq", train=262_144),
+               engine="fbpq", train=131_072, ref_books=True),
     "c2": dict(n=10_000_000, dim=128, ncomp=4096, t=4096, m=8, k=256, nq=10_000, L=10_000, topk=100,
-               engine="hbpq", train=262_144),
+               engine="hbpq", train=131_072, ref_books=True),
     # billion-scale (BASELINE configs[4]) on one GPU: streamed build, 16,384 components
     "c4": dict(n=1_000_000_000, dim=128, ncomp=16384, t=16384, m=8, k=256, nq=10_000, L=10_000, topk=100,
                engine="fbpq", train=1_048_576, stream=True),
@@ -82,6 +84,8 @@ def build_workload(cfg, device, rank=0):
                     tables=tables)
         return dix, q, (lambda: host)
     t0 = time.time()
+    if cfg.get("ref_books"):
+        return build_ref_books_workload(cfg, device, rank, t0)
     if cfg.get("normalized"):
         centt = datagen.normalized_centres_torch(cfg["ncomp"], cfg["dim"], device)
 
@@ -142,6 +146,53 @@ def build_workload(cfg, device, rank=0):
         f"{int((torch.diff(dix.offsets.long() & 0xFFFFFFFF) > 0).sum())}")
     def host():
         """Host copy of the index for the CPU baseline (built on demand)."""
+        h = dict(c1=c1, c2=c2, offsets=(dix.offsets.cpu().numpy().view(np.uint32)).astype(np.int64),
+                 ids=dix.ids.cpu().numpy().view(np.uint32), codes=dix.codes.cpu().numpy(), **host_books)
+        if cfg["engine"] != "hbpq":
+            h["tables"] = (dix.cn1.cpu().numpy(), dix.cn2.cpu().numpy(), dix.fine_norms.cpu().numpy(),
+                           dix.cross1.cpu().numpy(), dix.cross2.cpu().numpy())
+        return h
+
+    return dix, q, host
+
+
+def build_ref_books_workload(cfg, device, rank, t0):
+    """c1/c2: the reference-trained codebooks (tests/golden/c1_books.npz) and
+    the blocked numpy base/query stream (datagen.clipped_mixture_blocked), i.e.
+    the same vectors the --impl reference arm encodes with bilayerpq; encoding
+    and packing run on the device (encode.build_index)."""
+    import torch
+
+    from paper_1404_1831_b200 import datagen, encode
+
+    bk = np.load(ROOT / "tests" / "golden" / "c1_books.npz")
+    c1, c2, books = bk["c1"], bk["c2"], bk["books"]
+    cent = datagen.mixture_centres(cfg["ncomp"], cfg["dim"])
+    base_h = datagen.clipped_mixture_blocked(cfg["n"], cfg["dim"], cfg["ncomp"], datagen.SEED_BASE, centres=cent)
+    log(f"[setup] base drawn on the host in {time.time() - t0:.1f}s")
+    base = torch.empty((cfg["n"], cfg["dim"]), dtype=torch.float32, device=device)
+    step = 1 << 22
+    for s0 in range(0, cfg["n"], step):
+        base[s0:s0 + step].copy_(torch.from_numpy(base_h[s0:s0 + step]))
+    del base_h
+    host_books = dict(books=books)
+    if cfg["engine"] == "hbpq":
+        from paper_1404_1831_b200 import train
+
+        bank1, bank2 = train.local_bank_for_bench(base, c1, c2, books, cfg, device)
+        dix = encode.build_hbpq_index(base, c1, c2, bank1, bank2, device=device)
+        host_books = dict(bank1=bank1, bank2=bank2)
+    else:
+        dix = encode.build_index(base, c1, c2, books, device=device)
+    del base
+    torch.cuda.empty_cache()
+    qh = datagen.clipped_mixture_block(0, cfg["dim"], cfg["ncomp"], datagen.SEED_QUERIES + 1000 * rank, cent,
+                                       cfg["nq"])
+    q = torch.from_numpy(qh).to(device)
+    log(f"[setup] index built in {time.time() - t0:.1f}s: N={dix.n} populated="
+        f"{int((torch.diff(dix.offsets.long() & 0xFFFFFFFF) > 0).sum())}")
+
+    def host():
         h = dict(c1=c1, c2=c2, offsets=(dix.offsets.cpu().numpy().view(np.uint32)).astype(np.int64),
                  ids=dix.ids.cpu().numpy().view(np.uint32), codes=dix.codes.cpu().numpy(), **host_books)
         if cfg["engine"] != "hbpq":
@@ -256,28 +307,54 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------- CPU baseline
-def cpu_search(host, engine, queries, L, k, threads):
+def _oracle_index(host):
     from oracle import oracle as orc
 
-    idx = orc.Index(host["c1"], host["c2"], host["offsets"], host["ids"], host["codes"], books=host.get("books"),
-                    bank1=host.get("bank1"), bank2=host.get("bank2"), tables=host.get("tables"))
-    t0 = time.perf_counter()
-    d, i, c, nc = orc.search_batch_c(idx, engine, queries, L, k, threads=threads)
-    return time.perf_counter() - t0, nc
+    return orc.Index(host["c1"], host["c2"], host["offsets"], host["ids"], host["codes"], books=host.get("books"),
+                     bank1=host.get("bank1"), bank2=host.get("bank2"), tables=host.get("tables"))
 
 
 def cpu_baseline(host, engine, queries_np, L, k, budget_s=20.0):
+    """The C oracle (oracle/bpq_oracle.c, a port of the reference search) on
+    all host threads over a bounded query sample; returns the cpu_baseline
+    block and the oracle's answers for the parity check."""
+    from oracle import oracle as orc
+
     threads = os.cpu_count() or 1
-    # calibrate on a small sample, then size the sample to ~budget_s
+    idx = _oracle_index(host)
     n0 = min(len(queries_np), max(threads, 16))
-    dt, _ = cpu_search(host, engine, queries_np[:n0], L, k, threads)
-    per_q = dt / n0
+    t0 = time.perf_counter()
+    orc.search_batch_c(idx, engine, queries_np[:n0], L, k, threads=threads)
+    per_q = (time.perf_counter() - t0) / n0
     n = int(min(len(queries_np), max(n0, budget_s / max(per_q, 1e-6))))
-    dt, nc = cpu_search(host, engine, queries_np[:n], L, k, threads)
-    return {"value": n / dt, "unit": "queries/s", "cores": threads, "kind": "port",
-            "sample": f"first {n} of {len(queries_np)} queries, same index, L={L}, k={k}, "
-                      f"C oracle (oracle/bpq_oracle.c) with {threads} POSIX threads",
-            "codes_per_s": float(nc.sum()) / dt}
+    t0 = time.perf_counter()
+    res = orc.search_batch_c(idx, engine, queries_np[:n], L, k, threads=threads)
+    dt = time.perf_counter() - t0
+    block = {"value": n / dt, "unit": "queries/s", "cores": threads, "kind": "port",
+             "sample": f"first {n} of {len(queries_np)} queries, same index, L={L}, k={k}, "
+                       f"C oracle (oracle/bpq_oracle.c) with {threads} POSIX threads",
+             "codes_per_s": float(res[3].sum()) / dt}
+    return block, res, idx, n
+
+
+def parity_block(got, want, idx, queries_np, L):
+    """SURVEY §8c(ii) on the oracle's sample: the GPU answers (through the
+    public API, host buffers) against the C oracle's, every mismatch
+    classified (oracle/parity.py)."""
+    from oracle import oracle as orc
+    from oracle.parity import classify
+
+    gd, gi, gc, gn = got
+    wd, wi, wc, wn = want
+    n = wd.shape[0]
+    q = queries_np[:n]
+    qn = np.einsum("ij,ij->i", q.astype(np.float64), q.astype(np.float64))
+    s = classify(gd[:n], gi[:n], gc[:n], wd, wi, wc, qn, got_ncand=None if gn is None else gn[:n], want_ncand=wn,
+                 orc=orc, index=idx, queries=q, L=L)
+    s["oracle"] = "C oracle (oracle/bpq_oracle.c) on the same index and queries"
+    s["contract"] = ("SURVEY 8c(ii): shared-id distances within 1e-4 rel (floor 1e-6|q|^2); differing ids only as "
+                     "k-th-distance near-ties (1e-4) or in cells within 1e-5 of the oracle's cutoff key")
+    return s
 
 
 def launches_per_step(dix, engine):
@@ -291,6 +368,33 @@ def launches_per_step(dix, engine):
 
 
 # ------------------------------------------------------------------------ run
+METRIC = "queries/s (batched search at fixed L, k)"
+
+
+def _config(args):
+    if args.config == "c0":
+        cfg = dict(name="c0", nq=1000, L=10_000, topk=100, engine="fbpq", m=8, t=64, n=100_000, dim=128, k=256)
+    else:
+        cfg = dict(CONFIGS[args.config], name=args.config)
+    if args.engine:
+        cfg["engine"] = args.engine
+    if args.L:
+        cfg["L"] = args.L
+    if args.k:
+        cfg["topk"] = args.k
+    if args.nq:
+        cfg["nq"] = args.nq
+    return cfg
+
+
+def _config_block(cfg, n, dim, t, m, kk, nq, args, world):
+    engine, L, k = cfg["engine"], cfg["L"], cfg["topk"]
+    workload = f"{cfg['name']}: {engine} N={n:,} D={dim} T={t} M={m}x{kk} nq={nq} L={L} k={k}"
+    return {"workload": workload, "engine": engine, "N": n, "D": dim, "T": t, "M": m, "nq": nq, "L": L, "k": k,
+            "parallelism": (f"shard{world}" if args.shard else f"replicas{args.gpus}" if world > 1 else "single"),
+            "l2": "flushed between timed steps (256 MiB write)"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -303,19 +407,31 @@ def main():
     ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--nq", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exact", action="store_true", help="FBPQ/Multi-D-ADC/HBPQ in the reference's exact "
+                    "operation order (no point term, no per-cell residual tables)")
     ap.add_argument("--shard", action="store_true",
                     help="shard the database by point id across the ranks (global budget, NCCL all-gather merge)")
     ap.add_argument("--phase-profile", action="store_true",
                     help="print per-phase cycle shares of the fused kernel (needs BPQ_LIB=...libbpq_b200_prof.so)")
     args = ap.parse_args()
 
-    import torch
-
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.impl == "reference" and rank != 0:
+    cfg = _config(args)
+    if args.exact:
+        os.environ["BPQ_FBPQ_EXACT"] = "1"  # DeviceIndex default (index.py)
+    if args.impl == "reference":
+        # the reference's own CPU search on this host (rank 0 only; no product code, no CUDA)
+        if rank == 0:
+            import bench_reference
+
+            bench_reference.run(args, cfg, METRIC, _config_block(cfg, cfg["n"], cfg["dim"], cfg["t"], cfg["m"],
+                                                                 cfg["k"], cfg["nq"], args, world))
         return
+
+    import torch
+
     if world > 1 or args.shard:
         import torch.distributed as dist
 
@@ -329,18 +445,6 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     device = torch.device("cuda", local_rank)
 
-    if args.config == "c0":
-        cfg = dict(name="c0", nq=1000, L=10_000, topk=100, engine="fbpq", m=8, t=64, n=100_000, dim=128)
-    else:
-        cfg = dict(CONFIGS[args.config], name=args.config)
-    if args.engine:
-        cfg["engine"] = args.engine
-    if args.L:
-        cfg["L"] = args.L
-    if args.k:
-        cfg["topk"] = args.k
-    if args.nq:
-        cfg["nq"] = args.nq
     engine, L, k = cfg["engine"], cfg["L"], cfg["topk"]
     searcher = None
     if args.shard:
@@ -352,38 +456,9 @@ def main():
     else:
         dix, q, host = build_workload(cfg, device, rank)
     nq = q.shape[0]
-    workload = (f"{cfg['name']}: {engine} N={dix.n:,} D={dix.dim} T={dix.t} M={dix.m}x{dix.k} "
-                f"nq={nq} L={L} k={k}")
-    config = {"workload": workload, "engine": engine, "N": dix.n, "D": dix.dim, "T": dix.t, "M": dix.m,
-              "nq": nq, "L": L, "k": k,
-              "parallelism": (f"shard{world}" if args.shard else f"replicas{args.gpus}" if world > 1 else "single"),
-              "l2": "flushed between timed steps (256 MiB write)"}
-    metric = "queries/s (batched search at fixed L, k)"
-
-    if args.impl == "reference":
-        qn = q.cpu().numpy()
-        hostd = host()
-        steps_v = []
-        for s in range(args.warmup + args.steps):
-            per = max(1, 64 // 1)
-            lo = (s * per) % max(1, nq - per)
-            dt, nc = cpu_search(hostd, engine, qn[lo:lo + per], L, k, os.cpu_count())
-            if s >= args.warmup:
-                steps_v.append((per, dt, float(nc.sum())))
-        tot_q = sum(x[0] for x in steps_v)
-        tot_t = sum(x[1] for x in steps_v)
-        v = tot_q / tot_t
-        line = {"impl": "reference", "metric": metric, "value": v, "unit": "queries/s", "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": config,
-                "cpu_baseline": {"value": v, "unit": "queries/s", "cores": os.cpu_count(), "kind": "port",
-                                 "sample": f"{steps_v[0][0]} queries per step (of {nq}), C port of the reference "
-                                           f"search (oracle/bpq_oracle.c), {os.cpu_count()} threads"},
-                "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-                "codes_per_s": sum(x[2] for x in steps_v) / tot_t}
-        print(json.dumps(line), flush=True)
-        return
+    config = _config_block(cfg, dix.n, dix.dim, dix.t, dix.m, dix.k, nq, args, world)
+    workload = config["workload"]
+    metric = METRIC
 
     from paper_1404_1831_b200.index import SearchResult
 
@@ -402,7 +477,8 @@ def main():
     counts = out.counts.cpu().numpy()
     if (counts < 0).any():
         raise RuntimeError(f"{int((counts < 0).sum())} queries hit the tie-plateau limit")
-    ncand = int(out.ncand.sum().item())
+    ncand_q = out.ncand.cpu().numpy()
+    ncand = int(ncand_q.sum())
     npop = int(popped.sum().item())
     if args.phase_profile:
         from paper_1404_1831_b200 import _lib
@@ -483,11 +559,14 @@ def main():
         e2e_ms = float(tt.item())
     e2e_v = qmul * nq * args.steps / (e2e_ms / 1e3)
 
-    # roofline of the fused traversal+scan kernel ((M+4) B per candidate + 16 B per popped
-    # cell; the FBPQ point-term scan reads 4 B more per candidate: code M + point term 4 + id 4)
+    # roofline of the fused traversal+scan kernel, SURVEY §8(d) bytes: (M+4) B per candidate (code + id)
+    # + 16 B per popped cell (an offsets pair, empty cells included).  The default FBPQ scan also reads a
+    # 4 B point term per candidate (not in the §8(d) numerator; reported separately).
     search_ms = float(np.mean(stage_ms[:, 2]))
-    per_cand = dix.m + 4 + (4 if engine == "fbpq" and not dix.fbpq_exact else 0)
-    alg_bytes = per_cand * ncand + 16 * npop
+    pt_bytes = 4 * ncand if engine == "fbpq" and not dix.fbpq_exact else 0
+    scan_bytes = (dix.m + 4) * ncand
+    cell_bytes = 16 * npop
+    alg_bytes = scan_bytes + cell_bytes
     achieved = alg_bytes / (search_ms / 1e3) / 1e9
     traffic = None
     try:  # dram bytes per launch of the same kernel from the committed ncu --set full capture
@@ -509,7 +588,12 @@ def main():
                      "frac": achieved / HBM_PEAK, "traffic": traffic,
                      "kernel": "search_kernel (fused traversal + scan + top-k)",
                      "peak_source": HBM_PEAK_SRC, "alg_bytes_per_launch": alg_bytes,
-                     "alg_bytes_formula": f"{per_cand} B/candidate + 16 B/popped cell"},
+                     "alg_bytes_formula": f"SURVEY 8(d): {dix.m + 4} B/candidate + 16 B/popped cell",
+                     "scan_bytes_per_launch": scan_bytes, "cell_offset_bytes_per_launch": cell_bytes,
+                     "point_term_bytes_per_launch": pt_bytes,
+                     "frac_incl_point_term": (alg_bytes + pt_bytes) / (search_ms / 1e3) / 1e9 / HBM_PEAK},
+        "fbpq_mode": ("exact (reference operation order)" if dix.fbpq_exact else "point term (+4 B/entry)")
+                     if engine == "fbpq" else None,
         "e2e": {"value": e2e_v, "unit": "queries/s", "h2d_bytes_per_step": int(q.numel() * 4),
                 "d2h_bytes_per_step": int(nq * k * 8 + nq * 4)},
         "gpu_launches": (launches_per_step(dix, engine) + (1 if searcher is not None else 0)) * args.steps,
@@ -517,7 +601,11 @@ def main():
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline and host is not None:
         try:
-            line["cpu_baseline"] = cpu_baseline(host(), engine, q.cpu().numpy(), L, k)
+            qnp = q.cpu().numpy()
+            block, want, oidx, n = cpu_baseline(host(), engine, qnp, L, k)
+            line["cpu_baseline"] = block
+            got = (od_h.numpy(), oi_h.numpy().view(np.uint32), oc_h.numpy(), ncand_q)
+            line["parity"] = parity_block(got, want, oidx, qnp, L)
         except Exception as e:  # the baseline is reported, never required
             line["cpu_baseline"] = {"error": repr(e)}
     if rank == 0:

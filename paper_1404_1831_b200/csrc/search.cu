@@ -5,15 +5,30 @@
 #include "search_impl.cuh"
 
 namespace bpq {
-void set_prof_buffer_e0(unsigned long long *);
-void set_prof_buffer_e1(unsigned long long *);
-void set_prof_buffer_e2(unsigned long long *);
-int launch_search_e0(const Index &, const float *, int64_t, int64_t, int64_t, int32_t, const SearchWorkspace &,
-                     float *, uint32_t *, int32_t *, int64_t *, int64_t *, cudaStream_t);
-int launch_search_e1(const Index &, const float *, int64_t, int64_t, int64_t, int32_t, const SearchWorkspace &,
-                     float *, uint32_t *, int32_t *, int64_t *, int64_t *, cudaStream_t);
-int launch_search_e2(const Index &, const float *, int64_t, int64_t, int64_t, int32_t, const SearchWorkspace &,
-                     float *, uint32_t *, int32_t *, int64_t *, int64_t *, cudaStream_t);
+unsigned long long *g_prof_buffer = nullptr;
+
+#define BPQ_DECL_INST(E, M)                                                                        \
+    template <>                                                                                    \
+    int launch_search_inst<E, M>(const Index &, const float *, int64_t, int64_t, int64_t, int32_t, \
+                                 const SearchWorkspace &, float *, uint32_t *, int32_t *, int64_t *, \
+                                 int64_t *, cudaStream_t);
+BPQ_DECL_INST(0, 8) BPQ_DECL_INST(0, 16) BPQ_DECL_INST(0, 0)
+BPQ_DECL_INST(1, 8) BPQ_DECL_INST(1, 16) BPQ_DECL_INST(1, 0)
+BPQ_DECL_INST(2, 8) BPQ_DECL_INST(2, 16) BPQ_DECL_INST(2, 0)
+
+template <int ENGINE>
+int dispatch_m(const Index &ix, const float *queries, int64_t q0, int64_t nq, int64_t budget,
+               int32_t k, const SearchWorkspace &ws, float *od, uint32_t *oi, int32_t *oc,
+               int64_t *on, int64_t *op, cudaStream_t s) {
+    switch (ix.M) {
+        case 8: return launch_search_inst<ENGINE, 8>(ix, queries, q0, nq, budget, k, ws, od, oi, oc, on, op, s);
+        case 16: return launch_search_inst<ENGINE, 16>(ix, queries, q0, nq, budget, k, ws, od, oi, oc, on, op, s);
+        case 2: case 4: case 6: case 10: case 12: case 14:
+            return launch_search_inst<ENGINE, 0>(ix, queries, q0, nq, budget, k, ws, od, oi, oc, on, op, s);
+    }
+    return fail(BPQ_ERR_UNSUPPORTED, "num_parts must be even and in [2, 16]");
+}
+
 namespace {
 // ------------------------------------------- stage mirrors: per-candidate scans
 __global__ void stage_scan_kernel(int engine, const int32_t *__restrict__ vis_i,
@@ -174,11 +189,11 @@ int launch_search(const Index &ix, int engine, const float *queries, int64_t q0,
     if (nq == 0) return BPQ_OK;
     switch (engine) {
         case BPQ_ENGINE_BASELINE:
-            return launch_search_e0(ix, queries, q0, nq, budget, k, ws, out_dist, out_ids, out_count, out_ncand, out_popped, stream);
+            return dispatch_m<BPQ_ENGINE_BASELINE>(ix, queries, q0, nq, budget, k, ws, out_dist, out_ids, out_count, out_ncand, out_popped, stream);
         case BPQ_ENGINE_FBPQ:
-            return launch_search_e1(ix, queries, q0, nq, budget, k, ws, out_dist, out_ids, out_count, out_ncand, out_popped, stream);
+            return dispatch_m<BPQ_ENGINE_FBPQ>(ix, queries, q0, nq, budget, k, ws, out_dist, out_ids, out_count, out_ncand, out_popped, stream);
         case BPQ_ENGINE_HBPQ:
-            return launch_search_e2(ix, queries, q0, nq, budget, k, ws, out_dist, out_ids, out_count, out_ncand, out_popped, stream);
+            return dispatch_m<BPQ_ENGINE_HBPQ>(ix, queries, q0, nq, budget, k, ws, out_dist, out_ids, out_count, out_ncand, out_popped, stream);
     }
     return fail(BPQ_ERR_INVALID, "unknown engine");
 }
@@ -266,11 +281,7 @@ int launch_traverse_stage(const double *sr1, const double *sr2, const int32_t *o
 
 // ------------------------------------------------------- C ABI: diagnostics
 extern "C" int bpq_debug_set_phase_buffer(unsigned long long *dev_counters) {
-    // every translation unit keeps its own pointer; set all of them
     bpq::g_prof_buffer = dev_counters;
-    bpq::set_prof_buffer_e0(dev_counters);
-    bpq::set_prof_buffer_e1(dev_counters);
-    bpq::set_prof_buffer_e2(dev_counters);
 #ifdef BPQ_PHASE_PROF
     return 1;
 #else

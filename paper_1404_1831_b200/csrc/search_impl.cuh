@@ -46,6 +46,16 @@
 #include "bpq_internal.cuh"
 
 namespace bpq {
+// phase-profiling counters (bpq_debug_set_phase_buffer), one for all TUs
+extern unsigned long long *g_prof_buffer;
+
+// launches one fused-search instantiation; each (engine, M) pair is defined
+// in its own translation unit (search_inst.cu) so the ptxas runs go parallel
+template <int ENGINE, int MT>
+int launch_search_inst(const Index &ix, const float *queries, int64_t q0, int64_t nq, int64_t budget,
+                       int32_t k, const SearchWorkspace &ws, float *out_dist, uint32_t *out_ids,
+                       int32_t *out_count, int64_t *out_ncand, int64_t *out_popped, cudaStream_t stream);
+
 namespace {
 
 constexpr int NT = kSearchThreads;
@@ -1997,7 +2007,6 @@ __global__ void __launch_bounds__(NT, BPQ_MINB) search_kernel(Args<KT, OffT> A) 
     }
 }
 
-unsigned long long *g_prof_buffer = nullptr;
 
 // dynamic shared memory: Smem | per-query table | sorted-key prefixes | top-k buffer
 size_t tk_offset(int tab_floats, int sr_smem, size_t kt_size) {
@@ -2134,19 +2143,6 @@ int launch_one(const Index &ix, const float *queries, int64_t q0, int64_t nq, in
         search_kernel<ENGINE, MT, float, uint32_t><<<n_cta, NT, smem, stream>>>(A);
     BPQ_CUDA_TRY(cudaGetLastError());
     return BPQ_OK;
-}
-
-template <int ENGINE>
-int dispatch_m(const Index &ix, const float *queries, int64_t q0, int64_t nq, int64_t budget,
-               int32_t k, const SearchWorkspace &ws, float *od, uint32_t *oi, int32_t *oc,
-               int64_t *on, int64_t *op, cudaStream_t s) {
-    switch (ix.M) {
-        case 8: return launch_one<ENGINE, 8>(ix, queries, q0, nq, budget, k, ws, od, oi, oc, on, op, s);
-        case 16: return launch_one<ENGINE, 16>(ix, queries, q0, nq, budget, k, ws, od, oi, oc, on, op, s);
-        case 2: case 4: case 6: case 10: case 12: case 14:
-            return launch_one<ENGINE, 0>(ix, queries, q0, nq, budget, k, ws, od, oi, oc, on, op, s);
-    }
-    return fail(BPQ_ERR_UNSUPPORTED, "num_parts must be even and in [2, 16]");
 }
 
 }  // namespace

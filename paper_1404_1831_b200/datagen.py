@@ -37,6 +37,63 @@ def clipped_mixture(n: int, dim: int, ncomp: int, seed: int, centres=None) -> np
     return np.clip(np.round(centres[j] + 20.0 * z), 0, 255).astype(np.float32)
 
 
+BLOCK = 1 << 20
+
+
+def clipped_mixture_block(b: int, dim: int, ncomp: int, seed: int, centres, rows: int | None = None) -> np.ndarray:
+    """numpy draw of block ``b`` (rows [b*2^20, (b+1)*2^20)) of a blocked
+    clipped-mixture stream: every block has its own generator seeded by
+    (seed, b), so a process pool can draw disjoint blocks and any two
+    processes (the GPU arm and the CPU reference arm of bench.py) produce
+    the same rows bit for bit.  ``rows`` truncates the block."""
+    rng = np.random.default_rng(np.random.SeedSequence((int(seed), int(b), 0xB200)))
+    n = BLOCK if rows is None else int(rows)
+    j = rng.integers(0, ncomp, BLOCK)[:n]  # full-block draws: a prefix is the same rows
+    z = rng.standard_normal((BLOCK, dim), dtype=np.float32)[:n]
+    out = centres[j].astype(np.float32)
+    out += np.float32(20.0) * z
+    np.round(out, out=out)
+    np.clip(out, 0, 255, out=out)
+    return out
+
+
+def clipped_mixture_blocked(n: int, dim: int, ncomp: int, seed: int, workers: int | None = None,
+                            centres=None) -> np.ndarray:
+    """Rows [0, n) of the blocked stream, drawn by a fork pool into one
+    shared buffer (10M x 128 f32 in a few seconds on a many-core host)."""
+    import mmap
+    import multiprocessing as mp
+    import os
+
+    if centres is None:
+        centres = mixture_centres(ncomp, dim)
+    nb = (n + BLOCK - 1) // BLOCK
+    buf = mmap.mmap(-1, max(n * dim * 4, 1))
+    out = np.frombuffer(buf, dtype=np.float32, count=n * dim).reshape(n, dim)
+    workers = max(1, min(nb, workers or os.cpu_count() or 1))
+
+    def run(blocks):
+        for b in blocks:
+            lo = b * BLOCK
+            hi = min(n, lo + BLOCK)
+            out[lo:hi] = clipped_mixture_block(b, dim, ncomp, seed, centres, hi - lo)
+
+    if workers == 1 or nb == 1:
+        run(range(nb))
+        return out
+    procs = []
+    ctx = mp.get_context("fork")
+    for w in range(workers):
+        p = ctx.Process(target=run, args=(range(w, nb, workers),))
+        p.start()
+        procs.append(p)
+    for p in procs:
+        p.join()
+        if p.exitcode != 0:
+            raise RuntimeError("data generation worker failed")
+    return out
+
+
 def clipped_mixture_torch(n: int, dim: int, ncomp: int, seed: int, device, centres=None, chunk=1 << 22):
     """Same distribution drawn on ``device`` with a seeded torch generator."""
     import torch

@@ -98,12 +98,40 @@ def test_c_batch_search_within_contract(c0, oracle):
     agrees with the reference up to near-ties."""
     idx = _c0_index(c0, oracle)
     q = c0["queries"][:50].astype(np.float32)
-    d, i, cnt, _ = oracle.search_batch_c(idx, "fbpq", q, 10_000, 100, threads=4)
-    want_i = c0["fbpq_L10000_k100_ids"][:50]
-    want_d = c0["fbpq_L10000_k100_d"][:50]
-    np.testing.assert_allclose(d, want_d, rtol=1e-4)
-    same = np.mean([len(set(a) & set(b)) / 100 for a, b in zip(i, want_i)])
-    assert same > 0.99
+    q = c0["queries"][:200].astype(np.float32)
+    d, i, cnt, nc = oracle.search_batch_c(idx, "fbpq", q, 10_000, 100, threads=4)
+    from oracle.parity import check
+
+    want_c = np.minimum(100, c0["fbpq_L10000_k100_ncand"][:200])
+    qn = np.einsum("ij,ij->i", q.astype(np.float64), q.astype(np.float64))
+    s = check(d, i, cnt, c0["fbpq_L10000_k100_d"][:200], c0["fbpq_L10000_k100_ids"][:200], want_c, qn,
+              got_ncand=nc, want_ncand=c0["fbpq_L10000_k100_ncand"][:200], orc=oracle, index=idx, queries=q,
+              L=10_000)
+    assert s["exact_lists"] > 0
+
+
+def test_parity_classifier_rejects_real_mismatches(c0, oracle):
+    """The §8c(ii) classifier: a far-away id swapped in, a wrong distance or
+    a count change without a boundary near-tie are all unclassified."""
+    from oracle.parity import classify
+
+    idx = _c0_index(c0, oracle)
+    q = c0["queries"][:20].astype(np.float32)
+    wd = c0["fbpq_L10000_k100_d"][:20].copy()
+    wi = c0["fbpq_L10000_k100_ids"][:20].copy()
+    wc = np.minimum(100, c0["fbpq_L10000_k100_ncand"][:20])
+    ctx = dict(orc=oracle, index=idx, queries=q, L=10_000)
+    assert classify(wd, wi, wc, wd, wi, wc, **ctx)["exact_lists"] == 20
+    gi = wi.copy()
+    gi[0, 3] = wi[1, 50] if wi[1, 50] not in wi[0] else wi[1, 60]  # an id from another query, mid-list
+    assert classify(wd, gi, wc, wd, wi, wc, **ctx)["unclassified"] == 1
+    gd = wd.copy()
+    gd[2, 10] *= 1.01
+    assert classify(gd, wi, wc, wd, wi, wc, **ctx)["unclassified"] == 1
+    gc = wc.copy()
+    gc[4] -= 1
+    s = classify(wd, wi, gc, wd, wi, wc, **ctx)
+    assert s["count_mismatch"] == 1
 
 
 def test_rotated_variants_match_reference(oracle):
