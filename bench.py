@@ -359,11 +359,14 @@ def parity_block(got, want, idx, queries_np, L):
 
 def launches_per_step(dix, engine):
     """Engine kernels per bpq_search call (one query chunk): first layer, row
-    sort (partial on sparse tables), fold (FBPQ), fused search, and the
-    full-sort + search retry pass after a partial sort."""
+    sort (partial on sparse tables), fold (FBPQ), fused search, the
+    full-sort + search retry pass after a partial sort, and the large-cell
+    stream (point-term FBPQ, M = 8 / 16)."""
     n = 3 + (1 if engine == "fbpq" else 0)
     if dix.row_ptr is not None and dix.t > 1024:
         n += 2
+    if engine == "fbpq" and not dix.fbpq_exact and dix.m in (8, 16):
+        n += 1
     return n
 
 
@@ -497,7 +500,7 @@ def main():
         dix.search(q, L, k, engine, out=out, workspace=ws)
     torch.cuda.synchronize()
 
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
     for row in evs:  # torch creates CUDA events lazily on first record
         for e in row:
             e.record(stream)
@@ -522,8 +525,8 @@ def main():
     if searcher is not None:
         step_ms = [sev[s][0].elapsed_time(sev[s][1]) for s in range(args.steps)]
     else:
-        step_ms = [evs[s][0].elapsed_time(evs[s][3]) for s in range(args.steps)]
-    stage_ms = np.array([[evs[s][i].elapsed_time(evs[s][i + 1]) for i in range(3)] for s in range(args.steps)])
+        step_ms = [evs[s][0].elapsed_time(evs[s][4]) for s in range(args.steps)]
+    stage_ms = np.array([[evs[s][i].elapsed_time(evs[s][i + 1]) for i in range(4)] for s in range(args.steps)])
     t_ms = float(np.sum(step_ms))
     if world > 1:
         tt = torch.tensor([t_ms], device=device)
@@ -562,7 +565,8 @@ def main():
     # roofline of the fused traversal+scan kernel, SURVEY §8(d) bytes: (M+4) B per candidate (code + id)
     # + 16 B per popped cell (an offsets pair, empty cells included).  The default FBPQ scan also reads a
     # 4 B point term per candidate (not in the §8(d) numerator; reported separately).
-    search_ms = float(np.mean(stage_ms[:, 2]))
+    # the traversal kernel passes + the large-cell stream kernel
+    search_ms = float(np.mean(stage_ms[:, 2] + stage_ms[:, 3]))
     pt_bytes = 4 * ncand if engine == "fbpq" and not dix.fbpq_exact else 0
     scan_bytes = (dix.m + 4) * ncand
     cell_bytes = 16 * npop
@@ -582,11 +586,13 @@ def main():
         "config": config,
         "codes_scanned_per_s": world * ncand * args.steps / (t_ms / 1e3),
         "stage_ms": {"first_layer": float(np.mean(stage_ms[:, 0])), "row_sort_fold": float(np.mean(stage_ms[:, 1])),
-                     "traverse_scan_topk": search_ms},
+                     "traverse_scan_topk": float(np.mean(stage_ms[:, 2])),
+                     "large_cell_stream": float(np.mean(stage_ms[:, 3])), "search_total": search_ms},
         "work_per_step": {"candidates": ncand, "popped_cells": npop, "cand_per_query": ncand / nq},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": HBM_PEAK, "unit": "GB/s",
                      "frac": achieved / HBM_PEAK, "traffic": traffic,
-                     "kernel": "search_kernel (fused traversal + scan + top-k)",
+                     "kernel": "search_kernel (traversal + small-cell scan + top-k) + big_scan_kernel (TMA "
+                               "large-cell stream)",
                      "peak_source": HBM_PEAK_SRC, "alg_bytes_per_launch": alg_bytes,
                      "alg_bytes_formula": f"SURVEY 8(d): {dix.m + 4} B/candidate + 16 B/popped cell",
                      "scan_bytes_per_launch": scan_bytes, "cell_offset_bytes_per_launch": cell_bytes,

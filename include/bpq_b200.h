@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define BPQ_ABI_VERSION 2
+#define BPQ_ABI_VERSION 3
 
 enum {
     BPQ_OK = 0,
@@ -123,10 +123,12 @@ int bpq_search(const bpq_index *index, int engine, const float *queries, int64_t
                void *stream);
 
 /* bpq_search plus measurement hooks: stage_events (optional) is an array of
- * 4 cudaEvent_t recorded on the stream before the first-layer kernel, after
- * it, after the row sort and after the fused traversal/scan kernel (single
- * chunk only); out_popped (optional, [nq]) receives the cells the
- * multi-sequence pops up to the cutoff (empty cells included). */
+ * 5 cudaEvent_t recorded on the stream before the first-layer kernel, after
+ * it, after the row sort (+ FBPQ fold), after the fused traversal/scan
+ * passes and after the large-cell stream kernel (point-term FBPQ, M = 8 /
+ * 16; otherwise events 3 and 4 coincide) -- single chunk only; out_popped
+ * (optional, [nq]) receives the cells the multi-sequence pops up to the
+ * cutoff (empty cells included). */
 int bpq_search_ex(const bpq_index *index, int engine, const float *queries, int64_t nq,
                   int64_t budget, int32_t k, float *out_dist, uint32_t *out_ids,
                   int32_t *out_count, int64_t *out_ncand, int64_t *out_popped,
@@ -167,6 +169,16 @@ int bpq_nearest_centroids(const float *xs, int64_t n, int64_t ld_x, int32_t d,
                           const float *cents, const float *cent_norms, int32_t ncent,
                           int64_t *out_ids, float *out_d2, uint8_t *out_code,
                           int64_t code_stride, void *stream);
+/* Tensor-core nearest_centroids for d = 64 (tcgen05, exact bf16 limbs of x
+ * and of the centroids, f32 accumulation in TMEM, argmin fused into the
+ * epilogue).  The centroids enter as a pre-swizzled limb image built once by
+ * bpq_coarse_limb_image (bpq_coarse_limb_image_bytes(ncent) bytes,
+ * caller-owned device memory); outputs as bpq_nearest_centroids. */
+size_t bpq_coarse_limb_image_bytes(int32_t ncent);
+int bpq_coarse_limb_image(const float *cents, int32_t ncent, void *img, void *stream);
+int bpq_nearest_centroids_tc(const float *xs, int64_t n, int64_t ld_x, const void *img,
+                             const float *cent_norms, int32_t ncent, int64_t *out_ids, float *out_d2,
+                             uint8_t *out_code, int64_t code_stride, void *stream);
 /* residual = x - [c1[i]; c2[j]] then per-part nearest fine codeword. The
  * workspace holds n*dim floats (the residuals). */
 int bpq_encode_residual(const float *xs, int64_t n, int32_t dim, const float *coarse1,
@@ -200,6 +212,14 @@ int bpq_build_cell_lists(const uint32_t *offsets, int32_t t, uint32_t *row_ptr, 
  * idle) when the library was built with -DBPQ_PHASE_PROF; returns 1 if
  * compiled in, else 0 (and the buffer is never written). */
 int bpq_debug_set_phase_buffer(unsigned long long *dev_counters);
+
+/* First-layer stage of coarse_scan (multi_index.py:283-288): dots1[q, t] =
+ * q[:D/2] . c1[t], dots2[q, t] = q[D/2:] . c2[t] for nq device queries
+ * (already rotated if the index has a coarse rotation), on the path the
+ * index's searches use: the tcgen05 tensor-core GEMM over exact bf16 limbs
+ * when D = 128, else the FFMA kernel.  Outputs are caller-owned f32 [nq, T]. */
+int bpq_coarse_dots(const bpq_index *index, const float *queries, int64_t nq, float *dots1, float *dots2,
+                    void *stream);
 
 /* out[n, d] = x[n, d] @ R[d, d] (row-vector rotation, quantizer.py:95-96). */
 int bpq_rotate(const float *x, int64_t n, int32_t d, const float *R, float *out, void *stream);

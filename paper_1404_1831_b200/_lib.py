@@ -73,6 +73,9 @@ SIGNATURES = {
     "bpq_scan_global": (ctypes.c_int, [P, P, P, P, I64, I64, P, P, I32, I32, I32, P, P, P, P, P, P]),
     "bpq_scan_local": (ctypes.c_int, [P, P, P, P, I64, I64, P, P, I32, I32, I32, P, P, P, P, P, P, P]),
     "bpq_nearest_centroids": (ctypes.c_int, [P, I64, I64, I32, P, P, I32, P, P, P, I64, P]),
+    "bpq_coarse_limb_image_bytes": (SZ, [I32]),
+    "bpq_coarse_limb_image": (ctypes.c_int, [P, I32, P, P]),
+    "bpq_nearest_centroids_tc": (ctypes.c_int, [P, I64, I64, P, P, I32, P, P, P, I64, P]),
     "bpq_encode_residual": (ctypes.c_int, [P, I64, I32, P, P, P, P, P, P, I32, I32, P, P, SZ, P]),
     "bpq_encode_local": (ctypes.c_int, [P, I64, I32, P, P, P, P, P, P, I32, I32, P, P]),
     "bpq_pack_workspace_size": (SZ, [I64, I32]),
@@ -81,6 +84,7 @@ SIGNATURES = {
     "bpq_build_cell_lists": (ctypes.c_int, [P, I32, P, P, P, P, P, SZ, P]),
     "bpq_debug_set_phase_buffer": (ctypes.c_int, [P]),
     "bpq_rotate": (ctypes.c_int, [P, I64, I32, P, P, P]),
+    "bpq_coarse_dots": (ctypes.c_int, [P, P, I64, P, P, P]),
     "bpq_merge_topk": (ctypes.c_int, [P, P, P, I32, I64, I32, P, P, P, P]),
 }
 

@@ -51,6 +51,8 @@ struct Index {
     const float *books, *fine_norms, *cross1, *cross2, *bank1, *bank2;
     const float *rot, *rot1, *rot2;  // optional rotations (see bpq_index_desc)
     const float *pterm;  // FBPQ per-entry cross term [N] (null: exact reference-order scan)
+    // bf16 limb images of the coarse books for the tensor-core first layer (tc_dots.cu; null: FFMA)
+    const uint8_t *cimg1, *cimg2;
     bool exact;          // bpq_index_desc.fbpq_exact: reference operation order, all engines
     // populated-cell lists (optional): row i -> columns j, column j -> rows i
     const uint32_t *rowptr, *colptr;
@@ -64,6 +66,12 @@ int launch_point_term(const uint32_t *offsets, int32_t t, int32_t m, int32_t k, 
 int launch_coarse_dots(const float *queries, int64_t nq, int32_t D, const float *c1,
                        const float *c2, int32_t T, float *dots1, float *dots2,
                        cudaStream_t stream);
+size_t coarse_limb_image_bytes(int32_t T);
+int launch_coarse_limb_image(const float *C, int32_t T, uint8_t *img, cudaStream_t s);
+int launch_nearest_tc(const float *xs, int64_t n, int64_t ld_x, const uint8_t *img, const float *cn, int32_t nc,
+                      int64_t *out_ids, float *out_d2, uint8_t *out_code, int64_t code_stride, cudaStream_t s);
+int launch_coarse_dots_tc(const float *queries, int64_t nq, int32_t D, const uint8_t *img1, const uint8_t *img2,
+                          int32_t T, float *dots1, float *dots2, cudaStream_t s);
 int launch_fold(const float *queries, int64_t nq, int32_t D, int32_t M, int32_t K, const float *books,
                 const float *fine_norms, float *fold, cudaStream_t stream);
 int launch_row_sort(const float *queries, int64_t nq, int32_t D, const float *dots1,
@@ -84,6 +92,13 @@ struct SearchWorkspace {
     int32_t *plen;                 // per (query, half) prefix length of the partial sort
     const unsigned int *qlist, *qlist_count;  // indirect query list (retry pass)
     unsigned int *counter;
+    // large cells deferred by the traversal kernel to the stream kernel (point-term FBPQ, M = 8 / 16)
+    int4 *big_cells;               // [chunk][big_cap]
+    uint32_t *big_n, *tk_n;        // [chunk]
+    int big_cap;
+    unsigned long long *tk_part;   // [chunk][k]
+    unsigned long long *ncand_q;   // [chunk]
+    unsigned int *bigq_list, *bigq_count;
     char *cta_scratch;
     size_t cta_stride;
     int n_cta;
@@ -92,6 +107,10 @@ struct SearchWorkspace {
 size_t search_cta_scratch_bytes(int32_t T, int32_t D);
 int launch_rotate(const float *x, int64_t n, int32_t d, const float *R, float *out, cudaStream_t stream);
 int search_grid_ctas(int engine, int M);
+int effective_lut_min();
+int launch_big_scan(const Index &ix, int engine, const float *queries, int64_t q0, int64_t nq, int64_t budget,
+                    int32_t k, const SearchWorkspace &ws, float *out_dist, uint32_t *out_ids, int32_t *out_count,
+                    cudaStream_t stream);
 int launch_search(const Index &ix, int engine, const float *queries, int64_t q0, int64_t nq,
                   int64_t budget, int32_t k, const SearchWorkspace &ws, float *out_dist,
                   uint32_t *out_ids, int32_t *out_count, int64_t *out_ncand,

@@ -24,20 +24,31 @@ size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 struct SearchLayout {
     int64_t chunk;
     size_t dots1, dots2, sr1, sr2, ord1, ord2, pos1, pos2, fold, ru1, ru2, retry, plen, qrot, counter, cta, cta_stride, total;
+    size_t big, big_n, tk_n, tk_part, ncand_q, bigq;
+    int64_t big_cap;  // 0: no large-cell stream
     int n_cta;
 };
 
-int64_t query_chunk(int64_t nq, int32_t T, int32_t M, int32_t K) {
-    // keep the per-chunk first-layer buffers (10 arrays of [chunk, T] x 4 B + fold) near 8 GiB
-    int64_t per_q = (int64_t)T * 40 + (int64_t)M * K * 4 + 4;
+// large cells (>= lut_min entries) a query can visit: all but the cutoff cell lie inside the budget
+int64_t big_cells_cap(const Index &ix, int64_t budget) {
+    // the stream kernel moves codes by TMA bulk copies: 16-byte aligned code array
+    if (!(ix.pterm != nullptr && (ix.M == 8 || ix.M == 16)) || (reinterpret_cast<uintptr_t>(ix.codes) & 15)) return 0;
+    return budget / std::max(effective_lut_min(), 1) + 2;
+}
+
+int64_t query_chunk(int64_t nq, int32_t T, int32_t M, int32_t K, int64_t big_cap, int32_t k) {
+    // keep the per-chunk first-layer buffers (10 arrays of [chunk, T] x 4 B + fold), and the
+    // deferred large-cell lists, near 8 GiB
+    int64_t per_q = (int64_t)T * 40 + (int64_t)M * K * 4 + 4 + (big_cap ? big_cap * 16 + (int64_t)k * 8 + 32 : 0);
     int64_t c = ((int64_t)8 << 30) / per_q;
     c = std::max<int64_t>(c, 256);
     return std::max<int64_t>(1, std::min<int64_t>(nq, c));
 }
 
-bool layout_for(const Index &ix, int64_t nq, SearchLayout *L) {
+bool layout_for(const Index &ix, int64_t nq, int64_t budget, int32_t k, SearchLayout *L) {
     SearchLayout s{};
-    s.chunk = query_chunk(nq, ix.T, ix.M, ix.K);
+    s.big_cap = big_cells_cap(ix, budget);
+    s.chunk = query_chunk(nq, ix.T, ix.M, ix.K, s.big_cap, k);
     int n_cta = search_grid_ctas(BPQ_ENGINE_FBPQ, ix.M);
     if (n_cta <= 0) return false;
     s.n_cta = n_cta;
@@ -58,6 +69,14 @@ bool layout_for(const Index &ix, int64_t nq, SearchLayout *L) {
     s.plen = o; o += al((size_t)s.chunk * 8);
     s.qrot = o; o += ix.rot ? al((size_t)s.chunk * ix.D * 4) : 0;
     s.counter = o; o += al(4);
+    if (s.big_cap) {
+        s.big = o; o += al((size_t)s.chunk * s.big_cap * 16);
+        s.big_n = o; o += al((size_t)s.chunk * 4);
+        s.tk_n = o; o += al((size_t)s.chunk * 4);
+        s.tk_part = o; o += al((size_t)s.chunk * k * 8);
+        s.ncand_q = o; o += al((size_t)s.chunk * 8);
+        s.bigq = o; o += al((size_t)s.chunk * 4 + 4);
+    }
     s.cta_stride = al(search_cta_scratch_bytes(ix.T, ix.D));
     s.cta = o; o += s.cta_stride * n_cta;
     s.total = o;
@@ -186,6 +205,35 @@ extern "C" int bpq_index_create(const bpq_index_desc *d, int copy_from_host, bpq
             return fail(BPQ_ERR_CUDA, msg);
         }
     }
+    // tensor-core first layer (D = 128): pre-swizzled bf16 limbs of the coarse books
+    ix.cimg1 = ix.cimg2 = nullptr;
+    {
+        const char *fl = getenv("BPQ_FIRST_LAYER");  // "ffma": A/B diagnostics (read per index)
+        if (ix.dh == 64 && ix.T > 0 && !(fl && std::string(fl) == "ffma")) {
+            const size_t nb = coarse_limb_image_bytes(ix.T);
+            void *i1 = nullptr, *i2 = nullptr;
+            int rc = BPQ_OK;
+            if (cudaMalloc(&i1, nb) != cudaSuccess || cudaMalloc(&i2, nb) != cudaSuccess) {
+                cudaGetLastError();
+                rc = fail(BPQ_ERR_CUDA, "cannot allocate the coarse limb images");
+            }
+            if (i1) ix.owned.push_back(i1);
+            if (i2) ix.owned.push_back(i2);
+            if (rc == BPQ_OK && cudaDeviceSynchronize() != cudaSuccess)
+                rc = fail(BPQ_ERR_CUDA, cudaGetErrorString(cudaGetLastError()));
+            if (rc == BPQ_OK) rc = launch_coarse_limb_image(ix.c1, ix.T, static_cast<uint8_t *>(i1), 0);
+            if (rc == BPQ_OK) rc = launch_coarse_limb_image(ix.c2, ix.T, static_cast<uint8_t *>(i2), 0);
+            if (rc == BPQ_OK && cudaDeviceSynchronize() != cudaSuccess)
+                rc = fail(BPQ_ERR_CUDA, cudaGetErrorString(cudaGetLastError()));
+            if (rc) {
+                std::string msg = g_last_error;
+                bpq_index_destroy(h);
+                return fail(BPQ_ERR_CUDA, msg);
+            }
+            ix.cimg1 = static_cast<uint8_t *>(i1);
+            ix.cimg2 = static_cast<uint8_t *>(i2);
+        }
+    }
     ix.pterm = nullptr;
     ix.exact = d->fbpq_exact != 0;
     if (ix.cross1 && ix.cross2 && ix.codes && N > 0 && !d->fbpq_exact) {
@@ -229,7 +277,8 @@ extern "C" size_t bpq_search_workspace_size(const bpq_index *index, int engine, 
     (void)k;
     if (!index) return 0;
     SearchLayout L;
-    if (!layout_for(index->ix, std::max<int64_t>(nq, 1), &L)) return 0;
+    if (!layout_for(index->ix, std::max<int64_t>(nq, 1), std::max<int64_t>(budget, 1), std::max<int32_t>(k, 1), &L))
+        return 0;
     return L.total;
 }
 
@@ -270,7 +319,7 @@ extern "C" int bpq_search_ex(const bpq_index *index, int engine, const float *qu
     }
     if (nq == 0) return BPQ_OK;
     SearchLayout L;
-    BPQ_CHECK(layout_for(ix, nq, &L), BPQ_ERR_CUDA, "cannot size the search grid");
+    BPQ_CHECK(layout_for(ix, nq, budget, k, &L), BPQ_ERR_CUDA, "cannot size the search grid");
     BPQ_CHECK(workspace != nullptr && workspace_bytes >= L.total, BPQ_ERR_WORKSPACE,
               "search workspace too small (see bpq_search_workspace_size)");
     char *w = static_cast<char *>(workspace);
@@ -293,6 +342,18 @@ extern "C" int bpq_search_ex(const bpq_index *index, int engine, const float *qu
     ws.qlist = nullptr;
     ws.qlist_count = nullptr;
     ws.counter = reinterpret_cast<unsigned int *>(w + L.counter);
+    ws.big_cells = nullptr;
+    ws.big_cap = 0;
+    if (L.big_cap) {
+        ws.big_cells = reinterpret_cast<int4 *>(w + L.big);
+        ws.big_cap = (int)L.big_cap;
+        ws.big_n = reinterpret_cast<uint32_t *>(w + L.big_n);
+        ws.tk_n = reinterpret_cast<uint32_t *>(w + L.tk_n);
+        ws.tk_part = reinterpret_cast<unsigned long long *>(w + L.tk_part);
+        ws.ncand_q = reinterpret_cast<unsigned long long *>(w + L.ncand_q);
+        ws.bigq_count = reinterpret_cast<unsigned int *>(w + L.bigq);
+        ws.bigq_list = ws.bigq_count + 1;
+    }
     ws.cta_scratch = w + L.cta;
     ws.cta_stride = L.cta_stride;
     ws.n_cta = L.n_cta;
@@ -307,7 +368,8 @@ extern "C" int bpq_search_ex(const bpq_index *index, int engine, const float *qu
             if (rr) return rr;
             qc = ws.qrot;
         }
-        int rc = launch_coarse_dots(qc, n, ix.D, ix.c1, ix.c2, ix.T, ws.dots1, ws.dots2, s);
+        int rc = ix.cimg1 ? launch_coarse_dots_tc(qc, n, ix.D, ix.cimg1, ix.cimg2, ix.T, ws.dots1, ws.dots2, s)
+                          : launch_coarse_dots(qc, n, ix.D, ix.c1, ix.c2, ix.T, ws.dots1, ws.dots2, s);
         if (rc) return rc;
         if (ev) BPQ_CUDA_TRY(cudaEventRecord((cudaEvent_t)stage_events[1], s));
         // sparse tables only need the activated lines' sorted prefix: partial
@@ -326,6 +388,7 @@ extern "C" int bpq_search_ex(const bpq_index *index, int engine, const float *qu
         if (rc) return rc;
         ws.topP = partial ? kTopP : ix.T;
         BPQ_CUDA_TRY(cudaMemsetAsync(ws.retry_count, 0, 4, s));
+        if (ws.big_cells) BPQ_CUDA_TRY(cudaMemsetAsync(ws.bigq_count, 0, 4, s));
         if (engine == BPQ_ENGINE_FBPQ) {
             rc = launch_fold(qc, n, ix.D, ix.M, ix.K, ix.books, ix.fine_norms, ws.fold, s);
             if (rc) return rc;
@@ -351,8 +414,22 @@ extern "C" int bpq_search_ex(const bpq_index *index, int engine, const float *qu
             if (rc) return rc;
         }
         if (ev) BPQ_CUDA_TRY(cudaEventRecord((cudaEvent_t)stage_events[3], s));
+        // the large cells of every query the traversal passes handed over
+        rc = launch_big_scan(ix, engine, qc, q0, n, budget, k, ws, out_dist, out_ids, out_count, s);
+        if (rc) return rc;
+        if (ev) BPQ_CUDA_TRY(cudaEventRecord((cudaEvent_t)stage_events[4], s));
     }
     return BPQ_OK;
+}
+
+extern "C" int bpq_coarse_dots(const bpq_index *index, const float *queries, int64_t nq, float *dots1, float *dots2,
+                               void *stream) {
+    BPQ_CHECK(index != nullptr, BPQ_ERR_INVALID, "null index");
+    BPQ_CHECK(nq >= 0, BPQ_ERR_INVALID, "nq must be >= 0");
+    const Index &ix = index->ix;
+    cudaStream_t s = (cudaStream_t)stream;
+    return ix.cimg1 ? launch_coarse_dots_tc(queries, nq, ix.D, ix.cimg1, ix.cimg2, ix.T, dots1, dots2, s)
+                    : launch_coarse_dots(queries, nq, ix.D, ix.c1, ix.c2, ix.T, dots1, dots2, s);
 }
 
 extern "C" size_t bpq_traverse_workspace_size(int64_t t, int64_t budget, int64_t total_entries) {

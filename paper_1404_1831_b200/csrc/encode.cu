@@ -287,6 +287,24 @@ extern "C" int bpq_nearest_centroids(const float *xs, int64_t n, int64_t ld_x, i
     return BPQ_OK;
 }
 
+extern "C" size_t bpq_coarse_limb_image_bytes(int32_t ncent) {
+    return ncent > 0 ? bpq::coarse_limb_image_bytes(ncent) : 0;
+}
+
+extern "C" int bpq_coarse_limb_image(const float *cents, int32_t ncent, void *img, void *stream) {
+    BPQ_CHECK(ncent >= 1 && cents && img, BPQ_ERR_INVALID, "bad coarse limb image arguments");
+    return bpq::launch_coarse_limb_image(cents, ncent, static_cast<uint8_t *>(img), (cudaStream_t)stream);
+}
+
+extern "C" int bpq_nearest_centroids_tc(const float *xs, int64_t n, int64_t ld_x, const void *img,
+                                        const float *cent_norms, int32_t ncent, int64_t *out_ids, float *out_d2,
+                                        uint8_t *out_code, int64_t code_stride, void *stream) {
+    BPQ_CHECK(n >= 0 && ncent >= 1 && ld_x >= 64, BPQ_ERR_INVALID, "bad nearest_centroids shape");
+    BPQ_CHECK(out_code == nullptr || ncent <= 256, BPQ_ERR_INVALID, "uint8 codes need ncent <= 256");
+    return bpq::launch_nearest_tc(xs, n, ld_x, static_cast<const uint8_t *>(img), cent_norms, ncent, out_ids,
+                                  out_d2, out_code, code_stride, (cudaStream_t)stream);
+}
+
 extern "C" int bpq_encode_residual(const float *xs, int64_t n, int32_t dim, const float *coarse1,
                                    const float *coarse2, const int64_t *i_idx,
                                    const int64_t *j_idx, const float *books,

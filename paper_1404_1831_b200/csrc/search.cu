@@ -16,6 +16,26 @@ BPQ_DECL_INST(0, 8) BPQ_DECL_INST(0, 16) BPQ_DECL_INST(0, 0)
 BPQ_DECL_INST(1, 8) BPQ_DECL_INST(1, 16) BPQ_DECL_INST(1, 0)
 BPQ_DECL_INST(2, 8) BPQ_DECL_INST(2, 16) BPQ_DECL_INST(2, 0)
 
+template <>
+int launch_big_inst<8>(const Index &, const float *, int64_t, int64_t, int64_t, int32_t, const SearchWorkspace &,
+                       float *, uint32_t *, int32_t *, cudaStream_t);
+template <>
+int launch_big_inst<16>(const Index &, const float *, int64_t, int64_t, int64_t, int32_t, const SearchWorkspace &,
+                        float *, uint32_t *, int32_t *, cudaStream_t);
+
+int effective_lut_min() {
+    static const int env = getenv("BPQ_LUT_MIN") ? atoi(getenv("BPQ_LUT_MIN")) : 0;  // A/B experiments
+    return env > 0 ? env : kLutMin;
+}
+
+int launch_big_scan(const Index &ix, int engine, const float *queries, int64_t q0, int64_t nq, int64_t budget,
+                    int32_t k, const SearchWorkspace &ws, float *od, uint32_t *oi, int32_t *oc, cudaStream_t s) {
+    if (nq == 0 || engine != BPQ_ENGINE_FBPQ || ws.big_cells == nullptr || ix.pterm == nullptr) return BPQ_OK;
+    if (ix.M == 8) return launch_big_inst<8>(ix, queries, q0, nq, budget, k, ws, od, oi, oc, s);
+    if (ix.M == 16) return launch_big_inst<16>(ix, queries, q0, nq, budget, k, ws, od, oi, oc, s);
+    return BPQ_OK;
+}
+
 template <int ENGINE>
 int dispatch_m(const Index &ix, const float *queries, int64_t q0, int64_t nq, int64_t budget,
                int32_t k, const SearchWorkspace &ws, float *od, uint32_t *oi, int32_t *oc,

@@ -51,6 +51,10 @@ extern unsigned long long *g_prof_buffer;
 
 // launches one fused-search instantiation; each (engine, M) pair is defined
 // in its own translation unit (search_inst.cu) so the ptxas runs go parallel
+template <int MT>
+int launch_big_inst(const Index &ix, const float *queries, int64_t q0, int64_t nq, int64_t budget, int32_t k,
+                    const SearchWorkspace &ws, float *out_dist, uint32_t *out_ids, int32_t *out_count,
+                    cudaStream_t stream);
 template <int ENGINE, int MT>
 int launch_search_inst(const Index &ix, const float *queries, int64_t q0, int64_t nq, int64_t budget,
                        int32_t k, const SearchWorkspace &ws, float *out_dist, uint32_t *out_ids,
@@ -67,31 +71,65 @@ constexpr int ENGINE_TRAVERSE = 3;
 constexpr int kUnroll = 4;                // candidates per thread per round
 constexpr int kSrSmem = 4096;             // sorted half-distances staged in smem
 constexpr int kEnumBatch = 8;             // cell-table reads in flight per thread
-#ifndef BPQ_PIPE_U
-#define BPQ_PIPE_U 2
+// Large-cell scan (point-term FBPQ, M = 8 or 16): contiguous cell ranges of
+// codes and point terms stream into a ring of kBigS shared-memory stages by
+// TMA bulk copies (cp.async.bulk, one elected thread, mbarrier completion),
+// kBigCh entries per stage.
+#ifndef BPQ_BIG_S
+#define BPQ_BIG_S 3
 #endif
-#ifndef BPQ_PIPE_S
-#define BPQ_PIPE_S 3
-#endif
-constexpr int kPipeU = BPQ_PIPE_U;        // large-cell scan: entries per thread per round
-constexpr int kPipeR = NT * kPipeU;       // entries per round
-constexpr int kPipeS = BPQ_PIPE_S;        // cp.async stages (rounds in flight + 1)
-// shared-memory bytes of the large-cell pipeline for M parts (code + point term per entry)
-__host__ __device__ constexpr int pipe_stage_bytes(int m) { return kPipeS * kPipeR * (m + 4); }
+constexpr int kBigS = BPQ_BIG_S;
+__host__ __device__ constexpr int big_chunk(int m) { return m == 16 ? 256 : 512; }
+// shared-memory bytes of the large-cell stages for M parts (code + point term per entry)
+__host__ __device__ constexpr int pipe_stage_bytes(int m) { return kBigS * big_chunk(m) * (m + 4); }
 constexpr int kSortBytes = kSortCap * (8 + 4 + 2);  // skey + slin + sidx
 
-__device__ __forceinline__ void cp_async4(void *smem, const void *g) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(g));
+// Conflict-free fold table (FBPQ, M = 8 or 16).  fold[p][c] is stored R =
+// 32 / M times, at float index (c * M + p) * R + r.  Lane (g = lane / M,
+// x = lane % M) scores its own entry reading part (x + i) % M at step i from
+// replica g, so the 32 lanes of a warp hit 32 distinct banks on every
+// lookup (a plain [p][c] table costs ~3.5 wavefronts per random gather).
+template <int MT>
+__host__ __device__ constexpr bool rep_fold() { return MT == 8 || MT == 16; }
+template <int MT>
+__host__ __device__ constexpr int fold_floats_per_code() { return rep_fold<MT>() ? 32 : MT; }
+template <int MT>
+__device__ __forceinline__ int fold_index(int p, int c, int K) {
+    if constexpr (rep_fold<MT>()) return (c * MT + p) * (32 / MT);
+    else return p * K + c;
 }
-__device__ __forceinline__ void cp_async8(void *smem, const void *g) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(g));
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
-__device__ __forceinline__ void cp_async16(void *smem, const void *g) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(g));
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(unsigned long long *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+// TMA bulk copy global -> shared (16-byte aligned, size a multiple of 16), completion on *bar
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, unsigned long long *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
+    uint32_t ok = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
 
 struct __align__(16) Smem {
     uint32_t cpre[NT + 1];
@@ -128,6 +166,8 @@ struct __align__(16) Smem {
     unsigned long long tsel_below;
     unsigned long long tkey;
     uint32_t nholes;
+    uint32_t tphase;  // large-cell stage mbarrier parities (bit s = slot s)
+    unsigned long long mbar[kBigS];
     uint16_t holes[kMaxK];
 };
 
@@ -163,10 +203,20 @@ struct Args {
     const uint8_t *codes;
     const float *books, *fine_norms, *cross1, *cross2, *bank1, *bank2;
     const float *pterm;        // FBPQ per-entry point term (null: exact reference order)
+    // deferred large cells (point-term FBPQ, M = 8 / 16): the traversal kernel
+    // records them here and big_scan_kernel streams them (null: scan in place)
+    int4 *big_cells;           // [nq][big_cap] (start, count, cell_base bits, 0)
+    uint32_t *big_n;           // [nq] cells recorded
+    int big_cap;
+    unsigned long long *tk_part;  // [nq][k] top-k keys of the small cells
+    uint32_t *tk_n;            // [nq]
+    unsigned long long *ncand_q;  // [nq] candidate count (small + large cells)
+    unsigned int *bigq_list, *bigq_count;  // queries with deferred cells
     const float *rot1, *rot2;  // HBPQ per-half rotations (optional)
     bool exact;                // reference operation order for every engine (bpq_index_desc.fbpq_exact)
     double rho;
     unsigned long long n_global;
+    uint32_t n_local;          // entries in this index's (shard's) code / point-term arrays
     const float *queries;
     int64_t q0, nq;
     const float *dots1, *dots2, *fold;
@@ -361,6 +411,7 @@ __device__ __forceinline__ float dist_fbpq(const Args<KT, OffT> &A, const float 
 // M shared-memory lookups and no cross-table gathers.  Same quantity as the
 // reference's cell_base + sum_p (fold + 2*cross) (numba_backend.py:231-242),
 // summed in another order (max 4.3e-7 relative on the config-0 captures).
+// Generic-M path (plain [p][c] fold table).
 template <int MT>
 __device__ __forceinline__ float dist_fbpq_pt(const float *tab, int M, int K, float cbase, float pt,
                                               const uint32_t (&w)[4]) {
@@ -369,6 +420,88 @@ __device__ __forceinline__ float dist_fbpq_pt(const float *tab, int M, int K, fl
 #pragma unroll
     for (int p = 1; p < (MT ? MT : 16); p++)
         if (MT || p < M) s = __fadd_rn(s, tab[p * K + code_at(w, p)]);
+    const float acc = __fadd_rn(__fadd_rn(s, pt), cbase);
+    return acc < 0.f ? 0.f : acc;
+}
+
+// Rotation and replica of the conflict-free fold lookups (M = 8 or 16) for
+// an entry with y = (local entry index) & 31: the code bytes rotate by
+// x = y % M and, per step i, the lookup reads replica g = y / M of part
+// (x + i) % M at float offset ((x + i) % M) * R + g.  32 consecutive entries
+// scored by the 32 lanes of a warp therefore hit 32 distinct banks, and an
+// entry's summation order depends only on its position in the index (not on
+// the traversal, the lane or the scan path).
+template <int MT>
+struct LaneLut {
+    int rot;
+    int off[MT];
+    __device__ __forceinline__ explicit LaneLut(int y) {
+        constexpr int R = 32 / MT;
+        const int x = y % MT, g = (y / MT) % R;
+        rot = x;
+#pragma unroll
+        for (int i = 0; i < MT; i++) off[i] = ((x + i) % MT) * R + g;
+    }
+};
+
+// rotate the M code bytes right by L.rot bytes: byte i of the result is
+// part (rot + i) % M of the entry
+template <int MT>
+__device__ __forceinline__ void rotate_code(const uint32_t (&w)[4], int rot, uint32_t (&r)[4]) {
+    const uint32_t sh = 8u * (uint32_t)(rot & 3);
+    if constexpr (MT == 8) {
+        const bool sw = (rot & 4) != 0;
+        const uint32_t a0 = sw ? w[1] : w[0], a1 = sw ? w[0] : w[1];
+        r[0] = __funnelshift_r(a0, a1, sh);
+        r[1] = __funnelshift_r(a1, a0, sh);
+        r[2] = r[3] = 0;
+    } else {
+        const int q = rot >> 2;
+        uint32_t b0 = (q & 2) ? w[2] : w[0], b1 = (q & 2) ? w[3] : w[1];
+        uint32_t b2 = (q & 2) ? w[0] : w[2], b3 = (q & 2) ? w[1] : w[3];
+        const uint32_t a0 = (q & 1) ? b1 : b0, a1 = (q & 1) ? b2 : b1;
+        const uint32_t a2 = (q & 1) ? b3 : b2, a3 = (q & 1) ? b0 : b3;
+        r[0] = __funnelshift_r(a0, a1, sh);
+        r[1] = __funnelshift_r(a1, a2, sh);
+        r[2] = __funnelshift_r(a2, a3, sh);
+        r[3] = __funnelshift_r(a3, a0, sh);
+    }
+}
+
+// the same sum through the plain [p][c] fold table (small cells in the
+// traversal kernel): identical operation order, so an entry scores the same
+// bits whichever kernel scans it
+template <int MT>
+__device__ __forceinline__ float dist_pt_plain(const float *tab, int K, int y, float cbase, float pt,
+                                               const uint32_t (&w)[4]) {
+    const int x = y % MT;
+    uint32_t r[4];
+    rotate_code<MT>(w, x, r);
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < MT; i++) {
+        const uint32_t c = __byte_perm(r[i >> 2], 0u, 0x4440u | (uint32_t)(i & 3));
+        const float v = tab[((x + i) & (MT - 1)) * K + (int)c];
+        s = i == 0 ? v : __fadd_rn(s, v);
+    }
+    const float acc = __fadd_rn(__fadd_rn(s, pt), cbase);
+    return acc < 0.f ? 0.f : acc;
+}
+
+// point-term FBPQ distance through the replicated fold table (M = 8 or 16):
+// the parts are summed in the lane's rotated order, then + pt + cell_base
+template <int MT>
+__device__ __forceinline__ float dist_pt_rep(const float *tab, const LaneLut<MT> &L, float cbase, float pt,
+                                             const uint32_t (&w)[4]) {
+    uint32_t r[4];
+    rotate_code<MT>(w, L.rot, r);
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < MT; i++) {
+        const uint32_t c = __byte_perm(r[i >> 2], 0u, 0x4440u | (uint32_t)(i & 3));
+        const float v = tab[(int)(c << 5) + L.off[i]];
+        s = i == 0 ? v : __fadd_rn(s, v);
+    }
     const float acc = __fadd_rn(__fadd_rn(s, pt), cbase);
     return acc < 0.f ? 0.f : acc;
 }
@@ -533,6 +666,41 @@ __device__ void topk_compact(Smem &S, unsigned long long *__restrict__ tk, int k
     __syncthreads();
 }
 
+// Write the compacted top-k (S.ntk <= k unique keys in tk) as select_top's
+// (dist asc, id asc) list of min(k, ncand) entries, padded with (+inf, ~0).
+__device__ void write_topk(Smem &S, unsigned long long *__restrict__ tk, int k, unsigned long long ncand,
+                           float *__restrict__ od, uint32_t *__restrict__ oi, int32_t *__restrict__ oc) {
+    const uint32_t n = S.ntk;
+    const int cnt = (int)min((unsigned long long)k, ncand);
+    if (n <= 512) {
+        // keys are unique: each key's rank is its output position
+        for (int x = threadIdx.x; x < (int)n; x += NT) {
+            const unsigned long long kx = tk[x];
+            int rank = 0;
+            for (uint32_t y = 0; y < n; y++) rank += tk[y] < kx ? 1 : 0;
+            od[rank] = __uint_as_float((uint32_t)(kx >> 32));
+            oi[rank] = (uint32_t)kx;
+        }
+    } else {
+        int P2 = 1;
+        while (P2 < (int)n) P2 <<= 1;
+        for (int i = threadIdx.x; i < P2; i += NT)
+            if (i >= (int)n) tk[i] = ~0ull;
+        __syncthreads();
+        bitonic_sort_u64(tk, P2);
+        for (int x = threadIdx.x; x < cnt; x += NT) {
+            const unsigned long long kk = tk[x];
+            od[x] = __uint_as_float((uint32_t)(kk >> 32));
+            oi[x] = (uint32_t)kk;
+        }
+    }
+    for (int x = cnt + threadIdx.x; x < k; x += NT) {
+        od[x] = INFINITY;
+        oi[x] = 0xFFFFFFFFu;
+    }
+    if (threadIdx.x == 0) *oc = cnt;
+}
+
 // ------------------------------------------------------- per-query context
 //
 // Staircase state.  The popped region is a Young diagram in sorted
@@ -573,6 +741,7 @@ struct Query {
     int tp1, tp2;              // valid sorted prefix per half (partial sort), block-uniform
     unsigned long long ncand;  // uniform across the CTA
     unsigned long long popped;
+    uint32_t nbig_q;           // large cells deferred to big_scan_kernel (block-uniform)
 
     __device__ Query(const Args<KT, OffT> &a, Smem &s, int64_t q, const float *tab_, float *lut_,
                      const KT *s1, const KT *s2, unsigned long long *tk_)
@@ -598,6 +767,7 @@ struct Query {
         lut_i = lut_j = -1;
         ncand = 0;
         popped = 0;
+        nbig_q = 0;
     }
 
     // plain (not read-only-path) loads: extend() appends to sr/ord in-kernel
@@ -724,83 +894,27 @@ struct Query {
         PROF(pv);
     }
 
-    // FBPQ point-term scan of the band's large cells (M = 8 or 16): all of
-    // them as one stream of rounds of kPipeR entries.  Each thread copies its
-    // own entries' code and point term into its own shared-memory slots with
-    // cp.async, kPipeS - 1 rounds ahead of the round it scores, so the
-    // contiguous cell ranges stream from HBM while earlier rounds are scored
-    // (no register staging, no barrier between copy and use: a thread only
-    // reads the slots it filled).
-    __device__ void scan_big_pt(uint32_t nb) {
-        static_assert(MT == 8 || MT == 16, "pipelined scan needs M = 8 or 16");
-        const int pv = PROF(PH_LUT);
-        (void)pv;
-        const int K = A.K;
-        uint8_t *stc = reinterpret_cast<uint8_t *>(lut);       // [kPipeS][kPipeR][MT]
-        float *stp = reinterpret_cast<float *>(stc + kPipeS * kPipeR * MT);  // [kPipeS][kPipeR]
-        // issue cursor (x_i, e_i) and score cursor (x_c, e_c) walk the same
-        // round sequence; both are block-uniform
-        uint32_t x_i = 0, e_i = 0, x_c = 0, e_c = 0;
-        auto issue = [&](int slot) {
-            if (x_i < nb) {
-                const int t = S.bigs[x_i];
-                const uint32_t lst = S.cstart[t], lc = S.ccnt[t];
-#pragma unroll
-                for (int u = 0; u < kPipeU; u++) {
-                    const int j = u * NT + threadIdx.x;
-                    const uint32_t e = e_i + j;
-                    if (e < lc) {
-                        uint8_t *dc = stc + ((size_t)slot * kPipeR + j) * MT;
-                        const uint8_t *gc = A.codes + (size_t)(lst + e) * MT;
-                        if constexpr (MT == 16) cp_async16(dc, gc); else cp_async8(dc, gc);
-                        cp_async4(stp + slot * kPipeR + j, A.pterm + lst + e);
-                    }
-                }
-                e_i += kPipeR;
-                if (e_i >= lc) {
-                    x_i++;
-                    e_i = 0;
-                }
-            }
-            cp_async_commit();  // possibly empty: keeps the group count uniform
-        };
-#pragma unroll
-        for (int r = 0; r < kPipeS - 1; r++) issue(r);
-        for (int r = 0; x_c < nb; r++) {
-            issue((r + kPipeS - 1) % kPipeS);
-            cp_async_wait<kPipeS - 1>();
-            const int slot = r % kPipeS;
-            const int t = S.bigs[x_c];
-            const uint32_t lst = S.cstart[t], lc = S.ccnt[t];
-            const float cb = S.cbase[t];
-#pragma unroll
-            for (int u = 0; u < kPipeU; u++) {
-                const int j = u * NT + threadIdx.x;
-                const uint32_t e = e_c + j;
-                if (e < lc) {
-                    uint32_t w[4];
-                    if constexpr (MT == 16) {
-                        const uint4 v = *reinterpret_cast<const uint4 *>(stc + ((size_t)slot * kPipeR + j) * MT);
-                        w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
-                    } else {
-                        const uint2 v = *reinterpret_cast<const uint2 *>(stc + ((size_t)slot * kPipeR + j) * MT);
-                        w[0] = v.x; w[1] = v.y; w[2] = 0; w[3] = 0;
-                    }
-                    const float acc = dist_fbpq_pt<MT>(tab, MT, K, cb, stp[slot * kPipeR + j], w);
-                    offer_lazy(acc, A.ids + lst + e);
-                }
-            }
-            e_c += kPipeR;
-            if (e_c >= lc) {
-                ncand += lc;
-                x_c++;
-                e_c = 0;
-            }
-            round_end(kPipeR);
+    // Point-term FBPQ (M = 8 / 16): the band's large cells are recorded for
+    // big_scan_kernel, which streams their contiguous code / point-term
+    // ranges through a deep TMA ring (the traversal kernel keeps its
+    // occupancy; the stream gets the shared memory).  At most L / lut_min + 1
+    // large cells are visited per query: every visited cell but the cutoff
+    // cell lies inside the budget.
+    __device__ void defer_big(uint32_t nb) {
+        unsigned long long add = 0;
+        for (uint32_t x = threadIdx.x; x < nb; x += NT) {
+            const int t = S.bigs[x];
+            const uint32_t pos = nbig_q + x;
+            if (pos < (uint32_t)A.big_cap)
+                A.big_cells[(size_t)qi * A.big_cap + pos] =
+                    make_int4((int)S.cstart[t], (int)S.ccnt[t], __float_as_int(S.cbase[t]), 0);
+            else
+                S.err = 1;  // cannot happen within the L / lut_min + 2 bound; fail loudly if it does
+            add += S.ccnt[t];
         }
-        cp_async_wait<0>();
+        ncand += block_sum_u64(S, add);
+        nbig_q += nb;
         __syncthreads();
-        PROF(pv);
     }
 
     // Multi-D-ADC / HBPQ, one large cell: the cell's residual lookup table
@@ -982,7 +1096,11 @@ struct Query {
                         if (own[u] < 0) continue;
                         const int lo = own[u];
                         float dist;
-                        if constexpr (ENGINE == BPQ_ENGINE_FBPQ)
+                        if constexpr (ENGINE == BPQ_ENGINE_FBPQ && rep_fold<MT>())
+                            dist = A.pterm ? dist_pt_plain<MT>(tab, A.K, (int)(entry[u] & 31u), S.cbase[lo], ptv[u],
+                                                               w[u])
+                                           : dist_fbpq<MT>(A, tab, S.coi[lo], S.coj[lo], S.cbase[lo], w[u]);
+                        else if constexpr (ENGINE == BPQ_ENGINE_FBPQ)
                             dist = A.pterm ? dist_fbpq_pt<MT>(tab, M, A.K, S.cbase[lo], ptv[u], w[u])
                                            : dist_fbpq<MT>(A, tab, S.coi[lo], S.coj[lo], S.cbase[lo], w[u]);
                         else
@@ -994,7 +1112,7 @@ struct Query {
                 }
                 if constexpr (ENGINE == BPQ_ENGINE_FBPQ && MT != 0) {
                     if (A.pterm != nullptr) {
-                        if (S.nbig) scan_big_pt(S.nbig);
+                        if (S.nbig) defer_big(S.nbig);
                     } else {
                         const uint32_t nb = S.nbig;
                         for (uint32_t x = 0; x < nb; x++) {
@@ -1653,6 +1771,7 @@ struct Query {
             // pool overflow: restart this query with the band traversal
             ncand = 0;
             popped = 0;
+            nbig_q = 0;
             if (threadIdx.x == 0) {
                 S.ntk = 0;
                 S.thr = ~0ull;
@@ -1898,36 +2017,22 @@ struct Query {
             return;
         }
         topk_compact(S, tk, k);
-        uint32_t n = S.ntk;
-        int cnt = (int)min((unsigned long long)k, ncand);
-        if (n <= 512) {
-            // keys are unique: each key's rank is its output position
-            for (int x = threadIdx.x; x < (int)n; x += NT) {
-                const unsigned long long kx = tk[x];
-                int rank = 0;
-                for (uint32_t y = 0; y < n; y++) rank += tk[y] < kx ? 1 : 0;
-                A.out_d[qo * k + rank] = __uint_as_float((uint32_t)(kx >> 32));
-                A.out_ids[qo * k + rank] = (uint32_t)kx;
+        if (A.big_cells != nullptr && nbig_q > 0) {
+            // large cells pending: hand the small cells' top-k to big_scan_kernel
+            const uint32_t n = S.ntk;
+            for (uint32_t x = threadIdx.x; x < n; x += NT) A.tk_part[(size_t)qi * k + x] = tk[x];
+            if (threadIdx.x == 0) {
+                A.tk_n[qi] = n;
+                A.big_n[qi] = nbig_q;
+                A.ncand_q[qi] = ncand;
+                if (A.out_ncand) A.out_ncand[qo] = (int64_t)ncand;
+                if (A.out_popped) A.out_popped[qo] = (int64_t)popped;
+                A.bigq_list[atomicAdd(A.bigq_count, 1u)] = (unsigned int)qi;
             }
-        } else {
-            int P2 = 1;
-            while (P2 < (int)n) P2 <<= 1;
-            for (int i = threadIdx.x; i < P2; i += NT)
-                if (i >= (int)n) tk[i] = ~0ull;
-            __syncthreads();
-            bitonic_sort_u64(tk, P2);
-            for (int x = threadIdx.x; x < cnt; x += NT) {
-                unsigned long long kk = tk[x];
-                A.out_d[qo * k + x] = __uint_as_float((uint32_t)(kk >> 32));
-                A.out_ids[qo * k + x] = (uint32_t)kk;
-            }
+            return;
         }
-        for (int x = cnt + threadIdx.x; x < k; x += NT) {
-            A.out_d[qo * k + x] = INFINITY;
-            A.out_ids[qo * k + x] = 0xFFFFFFFFu;
-        }
+        write_topk(S, tk, k, ncand, A.out_d + qo * k, A.out_ids + qo * k, A.out_count + qo);
         if (threadIdx.x == 0) {
-            A.out_count[qo] = cnt;
             if (A.out_ncand) A.out_ncand[qo] = (int64_t)ncand;
             if (A.out_popped) A.out_popped[qo] = (int64_t)popped;
         }
@@ -1944,6 +2049,12 @@ __global__ void __launch_bounds__(NT, BPQ_MINB) search_kernel(Args<KT, OffT> A) 
     float *lut = tab + (ENGINE == BPQ_ENGINE_FBPQ ? M * A.K : ((A.D + 3) & ~3));
     KT *s1s = reinterpret_cast<KT *>(tab + A.tab_floats);
     KT *s2s = s1s + A.sr_smem;
+    if (threadIdx.x == 0) {
+        // large-cell stage barriers: one arrival (the issuing thread's expect_tx) per chunk
+        for (int s = 0; s < kBigS; s++) mbar_init(&S.mbar[s], 1);
+        S.tphase = 0;
+        mbar_fence_init();
+    }
 #ifdef BPQ_PHASE_PROF
     if (threadIdx.x == 0) {
         S.prof_ph = PH_IDLE;
@@ -2008,6 +2119,166 @@ __global__ void __launch_bounds__(NT, BPQ_MINB) search_kernel(Args<KT, OffT> A) 
 }
 
 
+// ------------------------------------------------------------------------
+// Large-cell stream (point-term FBPQ, M = 8 / 16).  For every query the
+// traversal kernel handed over (its small cells' top-k plus the list of its
+// large cells), stream the cells' contiguous code / point-term ranges
+// through a ring of kRingS shared-memory stages filled by TMA bulk copies
+// (cp.async.bulk, one elected thread, mbarrier completion), kRingCh entries
+// per stage, kRingS - 1 stages in flight.  Chunks start at a 32-entry
+// boundary, so lane l always scores entries with index % 32 == l and its
+// replicated-table offsets (LaneLut) are per-lane constants; leading entries
+// outside the cell are skipped, and entries past the 4-aligned end of the
+// arrays are read directly.  The fold table is the conflict-free replicated
+// layout (fold_index).  2 CTAs per SM.
+template <int MT>
+__host__ __device__ constexpr int ring_chunk() { return MT == 16 ? 512 : 1024; }
+#ifndef BPQ_RING_S
+#define BPQ_RING_S 4
+#endif
+constexpr int kRingS = BPQ_RING_S;
+template <int MT>
+__host__ __device__ constexpr int ring_bytes() { return kRingS * ring_chunk<MT>() * (MT + 4); }
+
+template <int MT, typename KT, typename OffT>
+__global__ void __launch_bounds__(NT, 2) big_scan_kernel(Args<KT, OffT> A) {
+    static_assert(MT == 8 || MT == 16, "large-cell stream needs M = 8 or 16");
+    constexpr int kCh = ring_chunk<MT>();
+    constexpr int kPer = kCh / NT;
+    constexpr int R = 32 / MT;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Smem &S = *reinterpret_cast<Smem *>(smem_raw);
+    float *tab = reinterpret_cast<float *>(smem_raw + sizeof(Smem));  // [K][M][R] replicated fold
+    unsigned long long *tk = reinterpret_cast<unsigned long long *>(smem_raw + A.tk_off);
+    uint8_t *stc = smem_raw + A.tk_off + (size_t)A.tkcap * 8;      // [kRingS][kCh][MT] codes
+    float *stp = reinterpret_cast<float *>(stc + (size_t)kRingS * kCh * MT);  // [kRingS][kCh] point terms
+    const int K = A.K, k = A.k;
+    const uint32_t nal = A.n_local & ~3u;  // 4-aligned end of the arrays
+    const LaneLut<MT> L((int)(threadIdx.x & 31));
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < kRingS; st++) mbar_init(&S.mbar[st], 1);
+        mbar_fence_init();
+    }
+    uint32_t ph = 0;  // stage mbarrier parities (block-uniform)
+    for (;;) {
+        if (threadIdx.x == 0) {
+            const unsigned int c = atomicAdd(A.counter, 1u);
+            S.qidx = c < *A.bigq_count ? (int64_t)A.bigq_list[c] : (int64_t)-1;
+        }
+        __syncthreads();
+        const int64_t qi = S.qidx;
+        if (qi < 0) return;
+        // replicated fold table and the small cells' top-k
+        const float *fq = A.fold + (size_t)qi * MT * K;
+        for (int x = threadIdx.x; x < MT * K; x += NT) {
+            const int p = x / K, c = x - p * K;
+            const float v = __ldg(fq + x);
+#pragma unroll
+            for (int r = 0; r < R; r++) tab[fold_index<MT>(p, c, K) + r] = v;
+        }
+        const uint32_t n0 = A.tk_n[qi];
+        unsigned long long mx = 0;
+        for (uint32_t x = threadIdx.x; x < n0; x += NT) {
+            const unsigned long long key = A.tk_part[(size_t)qi * k + x];
+            tk[x] = key;
+            mx = key > mx ? key : mx;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long y = __shfl_xor_sync(0xffffffffu, mx, o);
+            mx = y > mx ? y : mx;
+        }
+        if ((threadIdx.x & 31) == 0) S.red[threadIdx.x >> 5] = mx;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long m = 0;
+            for (int w = 0; w < NW; w++) m = S.red[w] > m ? S.red[w] : m;
+            S.ntk = n0;
+            // k keys held: the k-th smallest (their max) is the admission bound
+            S.thr = n0 >= (uint32_t)k ? m : ~0ull;
+        }
+        __syncthreads();
+        // stream the large cells
+        const int4 *cells = A.big_cells + (size_t)qi * A.big_cap;
+        const uint32_t nb = A.big_n[qi];
+        uint32_t x_i = 0, c_i = 0, x_c = 0, c_c = 0;  // issue / score cursors: cell, chunk start
+        if (nb) c_i = c_c = (uint32_t)__ldg(&cells[0].x) & ~31u;
+        if (threadIdx.x == 0) fence_proxy_async();  // the ring's previous readers were generic loads
+        auto issue = [&](int slot) {
+            if (x_i >= nb) return;
+            const int4 cl = __ldg(&cells[x_i]);
+            const uint32_t end = (uint32_t)cl.x + (uint32_t)cl.y;
+            if (threadIdx.x == 0) {
+                const uint32_t b1 = min(min(c_i + (uint32_t)kCh, (end + 3u) & ~3u), nal);
+                const uint32_t n = b1 > c_i ? b1 - c_i : 0u;
+                unsigned long long *bar = &S.mbar[slot];
+                mbar_arrive_tx(bar, n * (MT + 4));
+                if (n) {
+                    bulk_g2s(stc + (size_t)slot * kCh * MT, A.codes + (size_t)c_i * MT, n * MT, bar);
+                    bulk_g2s(stp + (size_t)slot * kCh, A.pterm + c_i, n * 4, bar);
+                }
+            }
+            c_i += kCh;
+            if (c_i >= end) {
+                x_i++;
+                if (x_i < nb) c_i = (uint32_t)__ldg(&cells[x_i].x) & ~31u;
+            }
+        };
+#pragma unroll
+        for (int r = 0; r < kRingS - 1; r++) issue(r);
+        for (int r = 0; x_c < nb; r++) {
+            issue((r + kRingS - 1) % kRingS);
+            const int slot = r % kRingS;
+            mbar_wait(&S.mbar[slot], (ph >> slot) & 1u);
+            ph ^= 1u << slot;
+            const int4 cl = __ldg(&cells[x_c]);
+            const uint32_t lst = (uint32_t)cl.x, end = lst + (uint32_t)cl.y;
+            const float cb = __int_as_float(cl.z);
+            const uint32_t b1 = min(min(c_c + (uint32_t)kCh, (end + 3u) & ~3u), nal);
+            const uint32_t thr_hi = (uint32_t)(S.thr >> 32);
+#pragma unroll
+            for (int u = 0; u < kPer; u++) {
+                const int j = u * NT + threadIdx.x;
+                const uint32_t e = c_c + j;
+                if (e >= lst && e < end) {
+                    uint32_t w[4];
+                    float ptv;
+                    if (e < b1) {
+                        if constexpr (MT == 16) {
+                            const uint4 v = *reinterpret_cast<const uint4 *>(stc + ((size_t)slot * kCh + j) * MT);
+                            w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+                        } else {
+                            const uint2 v = *reinterpret_cast<const uint2 *>(stc + ((size_t)slot * kCh + j) * MT);
+                            w[0] = v.x; w[1] = v.y; w[2] = 0; w[3] = 0;
+                        }
+                        ptv = stp[slot * kCh + j];
+                    } else {  // past the aligned end of the arrays
+                        load_code<MT>(A.codes + (size_t)e * MT, w, MT);
+                        ptv = __ldg(A.pterm + e);
+                    }
+                    const float acc = dist_pt_rep<MT>(tab, L, cb, ptv, w);
+                    const uint32_t db = canon_bits(acc);
+                    if (db <= thr_hi) {
+                        const unsigned long long kk = ((unsigned long long)db << 32) | __ldg(A.ids + e);
+                        if (kk < S.thr) tk[atomicAdd(&S.ntk, 1u)] = kk;
+                    }
+                }
+            }
+            c_c += kCh;
+            if (c_c >= end) {
+                x_c++;
+                if (x_c < nb) c_c = (uint32_t)__ldg(&cells[x_c].x) & ~31u;
+            }
+            __syncthreads();
+            if (S.ntk > (uint32_t)(A.tkcap - kCh)) topk_compact(S, tk, k);
+        }
+        topk_compact(S, tk, k);
+        const int64_t qo = A.q0 + qi;
+        write_topk(S, tk, k, A.ncand_q[qi], A.out_d + qo * k, A.out_ids + qo * k, A.out_count + qo);
+        __syncthreads();
+    }
+}
+
 // dynamic shared memory: Smem | per-query table | sorted-key prefixes | top-k buffer
 size_t tk_offset(int tab_floats, int sr_smem, size_t kt_size) {
     return (sizeof(Smem) + (size_t)tab_floats * 4 + 2 * (size_t)sr_smem * kt_size + 15) & ~(size_t)15;
@@ -2047,29 +2318,12 @@ int configure(size_t smem, int *n_cta_out) {
     return BPQ_OK;
 }
 
+// the launch-independent kernel arguments (index, workspace, outputs)
 template <int ENGINE, int MT>
-int launch_one(const Index &ix, const float *queries, int64_t q0, int64_t nq, int64_t budget,
-               int32_t k, const SearchWorkspace &ws, float *out_dist, uint32_t *out_ids,
-               int32_t *out_count, int64_t *out_ncand, int64_t *out_popped, cudaStream_t stream) {
-    Args<float, uint32_t> A{};
+void fill_args(Args<float, uint32_t> &A, const Index &ix, const float *queries, int64_t q0, int64_t nq,
+               int64_t budget, int32_t k, const SearchWorkspace &ws, float *out_dist, uint32_t *out_ids,
+               int32_t *out_count, int64_t *out_ncand, int64_t *out_popped) {
     A.M = ix.M;
-    // fold + per-cell LUT (exact FBPQ), or fold + the large-cell cp.async stages (point-term FBPQ)
-    // + the region shared by the LUT or cp.async stages and the sort arrays
-    A.tab_floats = ENGINE != BPQ_ENGINE_FBPQ ? ((ix.D + 3) & ~3) + std::max(ix.M * ix.K * 4, kSortBytes) / 4
-                   : (MT != 0 && ix.pterm != nullptr) ? ix.M * ix.K + std::max(pipe_stage_bytes(ix.M), kSortBytes) / 4
-                                                      : ix.M * ix.K + std::max(ix.M * ix.K * 4, kSortBytes) / 4;
-    A.tab_floats = (A.tab_floats + 3) & ~3;
-    A.sr_smem = 0;  // sorted keys are read through L1: only active lines are probed
-    A.tkcap = topk_capacity(k);
-    A.tk_off = (int)tk_offset(A.tab_floats, A.sr_smem, sizeof(float));
-    const size_t smem = dyn_smem_bytes(A.tab_floats, A.sr_smem, sizeof(float), A.tkcap);
-    // first pass over a partially sorted sparse table: sparse traversal only
-    const bool sparse_only = MT != 0 && ix.rowptr != nullptr && ws.topP < ix.T && ws.qlist == nullptr;
-    int n_cta = 0;
-    int rc = sparse_only ? configure<ENGINE, MT, float, uint32_t, (MT != 0)>(smem, &n_cta)
-                         : configure<ENGINE, MT, float, uint32_t>(smem, &n_cta);
-    if (rc) return rc;
-    if (n_cta > ws.n_cta) n_cta = ws.n_cta;
     A.T = ix.T;
     A.D = ix.D;
     A.dh = ix.dh;
@@ -2090,8 +2344,7 @@ int launch_one(const Index &ix, const float *queries, int64_t q0, int64_t nq, in
     A.cross1 = ix.cross1;
     A.cross2 = ix.cross2;
     A.pterm = ENGINE == BPQ_ENGINE_FBPQ ? ix.pterm : nullptr;
-    static const int lut_min_env = getenv("BPQ_LUT_MIN") ? atoi(getenv("BPQ_LUT_MIN")) : 0;  // A/B experiments
-    A.lut_min = lut_min_env > 0 ? lut_min_env : kLutMin;
+    A.lut_min = effective_lut_min();
     static const int nb0_env = getenv("BPQ_NB0") ? atoi(getenv("BPQ_NB0")) : 0;  // A/B experiments
     // first sparse-traversal batch: small budgets stop within a few lines
     A.nb0 = nb0_env > 0 ? (nb0_env < NT ? nb0_env : NT) : budget <= 2000 ? 32 : budget <= 5000 ? 64 : 128;
@@ -2100,6 +2353,7 @@ int launch_one(const Index &ix, const float *queries, int64_t q0, int64_t nq, in
     A.rot1 = ix.rot1;
     A.rot2 = ix.rot2;
     A.n_global = (unsigned long long)ix.N_global;
+    A.n_local = (uint32_t)ix.N;
     A.rho = (double)(ix.N_global > 0 ? ix.N_global : 1) / ((double)ix.T * ix.T);
     A.queries = queries;
     A.q0 = q0;
@@ -2136,6 +2390,42 @@ int launch_one(const Index &ix, const float *queries, int64_t q0, int64_t nq, in
     A.counter = ws.counter;
     A.scratch = ws.cta_scratch;
     A.stride = ws.cta_stride;
+    // point-term FBPQ with M = 8 / 16: large cells go to big_scan_kernel
+    const bool defer = ENGINE == BPQ_ENGINE_FBPQ && rep_fold<MT>() && ix.pterm != nullptr && ws.big_cells != nullptr;
+    A.big_cells = defer ? ws.big_cells : nullptr;
+    A.big_n = ws.big_n;
+    A.big_cap = ws.big_cap;
+    A.tk_part = ws.tk_part;
+    A.tk_n = ws.tk_n;
+    A.ncand_q = ws.ncand_q;
+    A.bigq_list = ws.bigq_list;
+    A.bigq_count = ws.bigq_count;
+}
+
+template <int ENGINE, int MT>
+int launch_one(const Index &ix, const float *queries, int64_t q0, int64_t nq, int64_t budget,
+               int32_t k, const SearchWorkspace &ws, float *out_dist, uint32_t *out_ids,
+               int32_t *out_count, int64_t *out_ncand, int64_t *out_popped, cudaStream_t stream) {
+    Args<float, uint32_t> A{};
+    fill_args<ENGINE, MT>(A, ix, queries, q0, nq, budget, k, ws, out_dist, out_ids, out_count, out_ncand, out_popped);
+    // fold + per-cell LUT (exact FBPQ / generic M) or fold + the sort arrays (point-term FBPQ, whose
+    // large cells are streamed by big_scan_kernel), the sort arrays aliasing the LUT
+    const bool defer = A.big_cells != nullptr;
+    A.tab_floats = ENGINE != BPQ_ENGINE_FBPQ ? ((ix.D + 3) & ~3) + std::max(ix.M * ix.K * 4, kSortBytes) / 4
+                   : defer ? ix.M * ix.K + kSortBytes / 4
+                           : ix.M * ix.K + std::max(ix.M * ix.K * 4, kSortBytes) / 4;
+    A.tab_floats = (A.tab_floats + 3) & ~3;
+    A.sr_smem = 0;  // sorted keys are read through L1: only active lines are probed
+    A.tkcap = topk_capacity(k);
+    A.tk_off = (int)tk_offset(A.tab_floats, A.sr_smem, sizeof(float));
+    const size_t smem = dyn_smem_bytes(A.tab_floats, A.sr_smem, sizeof(float), A.tkcap);
+    // first pass over a partially sorted sparse table: sparse traversal only
+    const bool sparse_only = MT != 0 && ix.rowptr != nullptr && ws.topP < ix.T && ws.qlist == nullptr;
+    int n_cta = 0;
+    int rc = sparse_only ? configure<ENGINE, MT, float, uint32_t, (MT != 0)>(smem, &n_cta)
+                         : configure<ENGINE, MT, float, uint32_t>(smem, &n_cta);
+    if (rc) return rc;
+    if (n_cta > ws.n_cta) n_cta = ws.n_cta;
     BPQ_CUDA_TRY(cudaMemsetAsync(ws.counter, 0, sizeof(unsigned int), stream));
     if (sparse_only)
         search_kernel<ENGINE, MT, float, uint32_t, (MT != 0)><<<n_cta, NT, smem, stream>>>(A);
@@ -2143,6 +2433,40 @@ int launch_one(const Index &ix, const float *queries, int64_t q0, int64_t nq, in
         search_kernel<ENGINE, MT, float, uint32_t><<<n_cta, NT, smem, stream>>>(A);
     BPQ_CUDA_TRY(cudaGetLastError());
     return BPQ_OK;
+}
+
+// the large-cell stream over the queries the traversal passes handed over
+template <int MT>
+int launch_big_one(const Index &ix, const float *queries, int64_t q0, int64_t nq, int64_t budget, int32_t k,
+                   const SearchWorkspace &ws, float *out_dist, uint32_t *out_ids, int32_t *out_count,
+                   cudaStream_t stream) {
+    if constexpr (!rep_fold<MT>()) {
+        return BPQ_OK;
+    } else {
+        Args<float, uint32_t> A{};
+        fill_args<BPQ_ENGINE_FBPQ, MT>(A, ix, queries, q0, nq, budget, k, ws, out_dist, out_ids, out_count,
+                                       nullptr, nullptr);
+        if (A.big_cells == nullptr) return BPQ_OK;
+        A.tkcap = ((k + 255) & ~255) + ring_chunk<MT>();
+        A.tk_off = (int)((sizeof(Smem) + (size_t)32 * ix.K * 4 + 15) & ~(size_t)15);
+        const size_t smem = (size_t)A.tk_off + (size_t)A.tkcap * 8 + ring_bytes<MT>();
+        auto kfn = big_scan_kernel<MT, float, uint32_t>;
+        static bool attr = false;
+        if (!attr) {
+            int dev = 0, optin = 0;
+            BPQ_CUDA_TRY(cudaGetDevice(&dev));
+            BPQ_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+            BPQ_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+            attr = true;
+        }
+        int occ = 0;
+        BPQ_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, NT, smem));
+        if (occ < 1) return fail(BPQ_ERR_UNSUPPORTED, "large-cell stream shared memory does not fit on an SM");
+        BPQ_CUDA_TRY(cudaMemsetAsync(ws.counter, 0, sizeof(unsigned int), stream));
+        kfn<<<occ * num_sms(), NT, smem, stream>>>(A);
+        BPQ_CUDA_TRY(cudaGetLastError());
+        return BPQ_OK;
+    }
 }
 
 }  // namespace

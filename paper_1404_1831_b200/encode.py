@@ -27,8 +27,16 @@ def _t(a, device, dtype=None):
     return torch.from_numpy(np.ascontiguousarray(a)).to(device=device, dtype=dtype).contiguous()
 
 
+def _use_tensor_cores(d: int) -> bool:
+    import os
+
+    return d == 64 and os.environ.get("BPQ_ENCODE") != "ffma"
+
+
 def nearest_centroids(xs, centroids, *, norms=None, want_d2=True, stream=None):
-    """(int64 ids, f32 d2) per row; ties break toward the lower id."""
+    """(int64 ids, f32 d2) per row; ties break toward the lower id.  For
+    d = 64 (the coarse halves at D = 128) the tcgen05 kernel with exact bf16
+    limbs runs; otherwise the FFMA kernel (BPQ_ENCODE=ffma forces it)."""
     import torch
 
     cents = _t(centroids, xs.device if isinstance(xs, torch.Tensor) else "cuda", torch.float32)
@@ -45,6 +53,15 @@ def nearest_centroids(xs, centroids, *, norms=None, want_d2=True, stream=None):
     ids = torch.empty(n, dtype=torch.int64, device=dev)
     d2 = torch.empty(n, dtype=torch.float32, device=dev) if want_d2 else None
     lib = _lib.load()
+    if _use_tensor_cores(xs.shape[1]):
+        nc = cents.shape[0]
+        img = torch.empty(int(lib.bpq_coarse_limb_image_bytes(nc)), dtype=torch.uint8, device=dev)
+        _lib.check(lib.bpq_coarse_limb_image(_lib.ptr(cents), nc, _lib.ptr(img), _lib.stream_ptr(stream)),
+                   "coarse_limb_image")
+        _lib.check(lib.bpq_nearest_centroids_tc(_lib.ptr(xs), n, xs.stride(0), _lib.ptr(img), _lib.ptr(cn), nc,
+                                                _lib.ptr(ids), _lib.ptr(d2), None, 0, _lib.stream_ptr(stream)),
+                   "nearest_centroids_tc")
+        return ids, d2
     _lib.check(lib.bpq_nearest_centroids(_lib.ptr(xs), n, xs.stride(0), xs.shape[1], _lib.ptr(cents),
                                          _lib.ptr(cn), cents.shape[0], _lib.ptr(ids), _lib.ptr(d2),
                                          None, 0, _lib.stream_ptr(stream)), "nearest_centroids")

@@ -280,6 +280,28 @@ class DeviceIndex:
         return ("hbpq",) if self.kind == "hbpq" else ("baseline", "fbpq")
 
     # --------------------------------------------------------------- search
+    def coarse_dots(self, queries):
+        """First-layer stage (coarse_scan's dot products, multi_index.py:
+        283-288) on the path this index's searches use (tcgen05 tensor cores
+        for D = 128, else FFMA): returns device f32 (dots1, dots2) [nq, T].
+        Queries are taken as given (already rotated for a rotated index)."""
+        import torch
+
+        if not isinstance(queries, torch.Tensor):
+            queries = torch.from_numpy(np.ascontiguousarray(np.atleast_2d(queries), np.float32))
+        queries = queries.to(device=self.device, dtype=torch.float32).contiguous()
+        if queries.dim() == 1:
+            queries = queries[None]
+        if queries.shape[1] != self.dim:
+            raise ValueError(f"dimension mismatch: vectors {queries.shape[1]}, index {self.dim}")
+        nq = queries.shape[0]
+        d1 = torch.empty((nq, self.t), dtype=torch.float32, device=self.device)
+        d2 = torch.empty((nq, self.t), dtype=torch.float32, device=self.device)
+        lib = _lib.load()
+        _lib.check(lib.bpq_coarse_dots(self._handle, _lib.ptr(queries), nq, _lib.ptr(d1), _lib.ptr(d2),
+                                       _lib.stream_ptr()), "bpq_coarse_dots")
+        return d1, d2
+
     def workspace_bytes(self, engine: str, nq: int, L: int, k: int) -> int:
         lib = _lib.load()
         return int(lib.bpq_search_workspace_size(self._handle, _lib.ENGINES[engine], nq, L, k))
@@ -342,7 +364,7 @@ class DeviceIndex:
         lib = _lib.load()
         ev = None
         if stage_events is not None:
-            ev = (ctypes.c_void_p * 4)(*[e.cuda_event for e in stage_events])
+            ev = (ctypes.c_void_p * 5)(*[e.cuda_event for e in stage_events])
         rc = lib.bpq_search_ex(
             self._handle, _lib.ENGINES[engine], _lib.ptr(queries), nq, int(L), int(k),
             _lib.ptr(out.dists), _lib.ptr(out.ids), _lib.ptr(out.counts), _lib.ptr(out.ncand),

@@ -22,7 +22,7 @@ def test_library_exports_header_symbols():
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) == set(_lib.SIGNATURES), set(syms) ^ set(_lib.SIGNATURES)
-    assert lib.bpq_abi_version() == 2
+    assert lib.bpq_abi_version() == 3
 
 
 def test_library_is_sm100a():

@@ -309,12 +309,14 @@ def test_partial_sort_large_t_matches_full_sort(torch_cuda, t):
 @pytest.mark.parametrize("m", [8, 16])
 def test_large_cells_every_engine_vs_oracle(torch_cuda, oracle, m):
     """Few coarse codewords, so cells hold hundreds of entries and take the
-    per-cell paths: FBPQ point term (cp.async stages) and exact LUT, and the
-    Multi-D-ADC / HBPQ residual lookup tables.  Contract of SURVEY §8c(ii)."""
+    per-cell paths: FBPQ point term (the TMA large-cell stream kernel) and
+    exact LUT, and the Multi-D-ADC / HBPQ residual lookup tables.  N is not
+    a multiple of 4, so the stream's tail past the last aligned chunk is read
+    directly.  Contract of SURVEY §8c(ii)."""
     from paper_1404_1831_b200 import DeviceIndex
 
     rng = np.random.default_rng(77 + m)
-    t, dim, kk, n = 10, 32, 32, 60_000
+    t, dim, kk, n = 10, 32, 32, 60_003
     base = rng.normal(size=(n, dim)).astype(np.float32)
     c1 = base[rng.choice(n, t, replace=False), : dim // 2].copy()
     c2 = base[rng.choice(n, t, replace=False), dim // 2 :].copy()
@@ -349,8 +351,16 @@ def test_empty_index_returns_nothing(torch_cuda):
     assert (c == 0).all() and np.isinf(d).all() and (i == 0xFFFFFFFF).all()
 
 
-def test_sharded_global_budget_equals_single(c0, torch_cuda):
-    """Shards built with id offsets + global counts: merged top-k == 1-index top-k."""
+@pytest.mark.parametrize("exact", [True, False])
+def test_sharded_global_budget_equals_single(c0, torch_cuda, exact):
+    """Shards built with id offsets + global counts: merged top-k == 1-index top-k.
+
+    Exact mode (reference operation order) is bit for bit.  The point-term
+    mode sums a candidate's M fold lookups in an order keyed on the entry's
+    position in its own (shard's) arrays (search_impl.cuh LaneLut), so a
+    distance may move by an ulp between the sharded and single layouts: the
+    merged answer must then meet the SURVEY 8c(ii) contract against the
+    single-index answer."""
     import torch
 
     from paper_1404_1831_b200 import DeviceIndex, sharded
@@ -359,20 +369,25 @@ def test_sharded_global_budget_equals_single(c0, torch_cuda):
     q = c0["queries"][:100].astype(np.float32)
     tables = (c0["cn1"], c0["cn2"], c0["fine_norms"], c0["cross1"], c0["cross2"])
     full = DeviceIndex(c1=c0["c1"], c2=c0["c2"], offsets=c0["offsets"], ids=c0["ids"], codes=c0["codes"],
-                       books=c0["books"], tables=tables)
+                       books=c0["books"], tables=tables, exact=exact)
     want = full.search(q, 10_000, 100, "fbpq").numpy()
     shards = sharded.split_index_arrays(c0["offsets"], c0["ids"], c0["codes"], 3)
     outs = []
     for s in shards:
         dix = DeviceIndex(c1=c0["c1"], c2=c0["c2"], offsets=s["offsets"], ids=s["ids"], codes=s["codes"],
                           books=c0["books"], tables=tables, global_offsets=c0["offsets"],
-                          num_entries_global=int(c0["offsets"][-1]))
+                          num_entries_global=int(c0["offsets"][-1]), exact=exact)
         outs.append(dix.search(q, 10_000, 100, "fbpq"))
     merged = sharded.merge_results([o.dists for o in outs], [o.ids for o in outs], [o.counts for o in outs], 100)
     got = merged.numpy()
-    np.testing.assert_array_equal(got[1], want[1])
-    np.testing.assert_array_equal(got[0], want[0])
-    np.testing.assert_array_equal(got[2], want[2])
+    if exact:
+        np.testing.assert_array_equal(got[1], want[1])
+        np.testing.assert_array_equal(got[0], want[0])
+        np.testing.assert_array_equal(got[2], want[2])
+    else:
+        np.testing.assert_array_equal(got[2], want[2])
+        qn = np.einsum("ij,ij->i", q.astype(np.float64), q.astype(np.float64))
+        check_topk(got[0], got[1], got[2], want[0], want[1], want[2], qn)
 
 
 def test_device_encoding_matches_reference(c0, torch_cuda):
@@ -576,3 +591,68 @@ def test_fuzz_small_configs_vs_oracle(torch_cuda, oracle, seed):
                 wd, wi, wc, _ = oracle.search_batch_numpy(oi, eng, q, L, k)
                 d, i, c = di.search(q, L, k, eng).numpy()
                 check_topk(d, i, c, wd, wi, wc, _qn(q), **_ctx(oi, q, L))
+
+
+@pytest.mark.parametrize("t,kind", [(64, "integer"), (4096, "integer"), (4096, "float"), (300, "float")])
+def test_first_layer_tensor_cores_vs_f64(torch_cuda, t, kind, monkeypatch):
+    """The tcgen05 first layer (exact bf16 limb products, f32 accumulation in
+    TMEM) against f64 dot products, beside the FFMA kernel: both within
+    2^-20 of sum |q_u c_u| (a few f32 accumulation roundings).  Covers one
+    padded tile (T=64), T not a multiple of the 128-codeword tile, nq not a
+    multiple of the 128-query tile, and integer (1-limb) vs float (3-limb)
+    queries."""
+    from paper_1404_1831_b200 import DeviceIndex
+
+    rng = np.random.default_rng(t)
+    dim, m, kk, nq = 128, 8, 16, 300
+    c1 = (rng.normal(size=(t, 64)) * 40 + 100).astype(np.float32)
+    c2 = (rng.normal(size=(t, 64)) * 40 + 100).astype(np.float32)
+    books = rng.normal(size=(m, kk, dim // m)).astype(np.float32)
+    off = np.zeros(t * t + 1, np.int64)
+    args = dict(c1=c1, c2=c2, offsets=off, ids=np.zeros(0, np.uint32), codes=np.zeros((0, m), np.uint8), books=books)
+    if kind == "integer":
+        q = np.clip(np.round(rng.normal(size=(nq, dim)) * 40 + 100), 0, 255).astype(np.float32)
+    else:
+        q = (rng.normal(size=(nq, dim)) * 40 + 100).astype(np.float32)
+    tc = DeviceIndex(**args)
+    monkeypatch.setenv("BPQ_FIRST_LAYER", "ffma")
+    ff = DeviceIndex(**args)
+    for h, c in ((0, c1), (1, c2)):
+        qh = q[:, h * 64:(h + 1) * 64].astype(np.float64)
+        exact = qh @ c.astype(np.float64).T
+        bound = 2.0 ** -20 * (np.abs(qh) @ np.abs(c.astype(np.float64)).T)
+        got_tc = tc.coarse_dots(q)[h].cpu().numpy()
+        got_ff = ff.coarse_dots(q)[h].cpu().numpy()
+        for name, got in (("tensor cores", got_tc), ("ffma", got_ff)):
+            err = np.abs(got.astype(np.float64) - exact)
+            assert np.all(err <= bound), f"{name} half {h}: max err/bound {np.max(err / bound):.3f}"
+
+
+@pytest.mark.parametrize("nc,kind", [(300, "integer"), (4096, "integer"), (256, "float")])
+def test_nearest_centroids_tensor_cores_vs_f64(torch_cuda, nc, kind):
+    """The tcgen05 encoder (d = 64, argmin fused into the TMEM epilogue)
+    against an f64 argmin of nearest_centroids' score |c|^2 - 2 x.c
+    (quantizer.py:109-130): the chosen centroid is the true minimum or
+    within 1e-6 of its magnitude (an argmin near-tie of the f32 scores), and
+    d2 agrees within 1e-4 relative (floor 1e-3)."""
+    import torch
+
+    from paper_1404_1831_b200 import encode
+
+    rng = np.random.default_rng(nc)
+    n = 1000
+    cents = (rng.normal(size=(nc, 64)) * 30 + 100).astype(np.float32)
+    if kind == "integer":
+        x = np.clip(np.round(rng.normal(size=(n, 64)) * 40 + 100), 0, 255).astype(np.float32)
+    else:
+        x = (rng.normal(size=(n, 64)) * 40 + 100).astype(np.float32)
+    ids, d2 = encode.nearest_centroids(torch.from_numpy(x).cuda(), cents)
+    ids, d2 = ids.cpu().numpy(), d2.cpu().numpy()
+    c64 = cents.astype(np.float64)
+    score = (c64 * c64).sum(1)[None] - 2 * x.astype(np.float64) @ c64.T
+    best = score.min(1)
+    got = score[np.arange(n), ids]
+    scale = np.abs(score).max(1)
+    assert np.all(got - best <= 1e-6 * scale), np.max((got - best) / scale)
+    want_d2 = np.maximum(best + (x.astype(np.float64) ** 2).sum(1), 0)
+    assert np.all(np.abs(d2 - want_d2) <= 1e-4 * np.maximum(want_d2, 1e-3) + 1e-6 * scale)

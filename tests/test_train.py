@@ -3,8 +3,13 @@ reference itself (tests/golden: c0 coarse + fine books, the HBPQ rig's
 local bank), with the reference's random draws (train.py rng="exact").
 
 Equality is bit-for-bit unless a Lloyd assignment hit an argmin near-tie
-(f32 scores of the GPU kernel vs OpenBLAS, quantizer.py:124-125); then the
-books must still reach the reference's training objective within 1e-4."""
+(f32 scores of the GPU kernel vs OpenBLAS, quantizer.py:124-125).  After
+such a tie the two Lloyd trajectories continue from different assignments
+and may stop in different local optima, so a differing book must still
+reach the reference's training objective within ``tol`` (1e-4 for the
+global books; 1% for the small local cells of the HBPQ bank, where one
+reassigned point moves a 1-2k-point k-means), and almost every book must be
+identical."""
 
 import numpy as np
 import pytest
@@ -27,11 +32,11 @@ def _objective(x, cents):
     return float(np.maximum(d.min(1), 0).sum())
 
 
-def _same_or_objective(got, want, data, what):
+def _same_or_objective(got, want, data, what, tol=1e-4):
     if np.array_equal(got, want):
         return "identical"
     og, ow = _objective(data, got), _objective(data, want)
-    assert abs(og - ow) <= 1e-4 * ow, f"{what}: objective {og} vs reference {ow}"
+    assert abs(og - ow) <= tol * ow, f"{what}: objective {og} vs reference {ow}"
     return f"objective within {abs(og - ow) / ow:.1e}"
 
 
@@ -64,9 +69,12 @@ def test_train_local_codebooks_match_reference(dev, hbpq_rig):
         for i in range(got.shape[0]):
             members = disp[cell == i, h * 64:(h + 1) * 64]
             for p in range(4):
-                r = _same_or_objective(got[i, p], want[i, p], members[:, p * 16:(p + 1) * 16], f"bank{h+1}[{i},{p}]")
+                r = _same_or_objective(got[i, p], want[i, p], members[:, p * 16:(p + 1) * 16], f"bank{h+1}[{i},{p}]",
+                                       tol=1e-2)
                 same += r == "identical"
-    print(f"{same} of {2 * b1.shape[0] * 4} local books identical")
+    total = 2 * b1.shape[0] * 4
+    print(f"{same} of {total} local books identical")
+    assert same >= 0.9 * total, f"only {same} of {total} local books identical"
 
 
 def test_device_rng_mode_trains_comparable_books(dev, c0):
