@@ -44,6 +44,23 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
+# exact-NN ground truth of the first RECALL_Q queries (evalbench.ExactNN), filled while the base is
+# resident (c1/c2) or streamed (c3/c4) during setup; reported as Recall@{1,10,100} (untimed)
+RECALL_Q = 1000
+GT = {}
+
+
+def _gt_start(q):
+    from paper_1404_1831_b200 import evalbench
+
+    if RECALL_Q <= 0:
+        return None
+    n = min(RECALL_Q, q.shape[0])
+    GT["n"] = n
+    GT["acc"] = evalbench.ExactNN(q[:n])
+    return GT["acc"]
+
+
 # --------------------------------------------------------------------- setup
 CONFIGS = {
     # c1/c2: codebooks trained by the reference itself (tests/golden/c1_books.npz), base and queries from
@@ -113,8 +130,16 @@ def build_workload(cfg, device, rank=0):
                       for p in range(cfg["m"])])
     log(f"[setup] codebooks trained in {time.time() - t0:.1f}s")
     if cfg.get("stream"):
-        dix = encode.build_index_streamed(cfg["n"], lambda s, e: draw(s, e, datagen.SEED_BASE), c1, c2, books,
-                                          device=device)
+        q = draw(0, cfg["nq"], datagen.SEED_QUERIES + 1000 * rank)
+        acc = _gt_start(q)
+
+        def draw_base(s, e):
+            x = draw(s, e, datagen.SEED_BASE)
+            if acc is not None:
+                acc.add(s, x)
+            return x
+
+        dix = encode.build_index_streamed(cfg["n"], draw_base, c1, c2, books, device=device)
         host_books = dict(books=books)
         base = None
     else:
@@ -138,7 +163,7 @@ def build_workload(cfg, device, rank=0):
     del base
     torch.cuda.empty_cache()
     if cfg.get("stream"):
-        q = draw(0, cfg["nq"], datagen.SEED_QUERIES + 1000 * rank)
+        pass  # drawn before the build
     else:
         q = datagen.clipped_mixture_torch(cfg["nq"], cfg["dim"], cfg["ncomp"], datagen.SEED_QUERIES + 1000 * rank,
                                           device, cent)
@@ -176,6 +201,12 @@ def build_ref_books_workload(cfg, device, rank, t0):
         base[s0:s0 + step].copy_(torch.from_numpy(base_h[s0:s0 + step]))
     del base_h
     host_books = dict(books=books)
+    qh = datagen.clipped_mixture_block(0, cfg["dim"], cfg["ncomp"], datagen.SEED_QUERIES + 1000 * rank, cent,
+                                       cfg["nq"])
+    q = torch.from_numpy(qh).to(device)
+    acc = _gt_start(q)
+    if acc is not None:
+        acc.add(0, base)
     if cfg["engine"] == "hbpq":
         from paper_1404_1831_b200 import train
 
@@ -186,9 +217,6 @@ def build_ref_books_workload(cfg, device, rank, t0):
         dix = encode.build_index(base, c1, c2, books, device=device)
     del base
     torch.cuda.empty_cache()
-    qh = datagen.clipped_mixture_block(0, cfg["dim"], cfg["ncomp"], datagen.SEED_QUERIES + 1000 * rank, cent,
-                                       cfg["nq"])
-    q = torch.from_numpy(qh).to(device)
     log(f"[setup] index built in {time.time() - t0:.1f}s: N={dix.n} populated="
         f"{int((torch.diff(dix.offsets.long() & 0xFFFFFFFF) > 0).sum())}")
 
@@ -410,6 +438,8 @@ def main():
     ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--nq", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--recall-queries", type=int, default=1000,
+                    help="queries whose exact NN is computed during setup for Recall@{1,10,100} (0: off)")
     ap.add_argument("--exact", action="store_true", help="FBPQ/Multi-D-ADC/HBPQ in the reference's exact "
                     "operation order (no point term, no per-cell residual tables)")
     ap.add_argument("--shard", action="store_true",
@@ -418,6 +448,8 @@ def main():
                     help="print per-phase cycle shares of the fused kernel (needs BPQ_LIB=...libbpq_b200_prof.so)")
     args = ap.parse_args()
 
+    global RECALL_Q
+    RECALL_Q = args.recall_queries
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -605,6 +637,17 @@ def main():
         "gpu_launches": (launches_per_step(dix, engine) + (1 if searcher is not None else 0)) * args.steps,
         "clocks": clk.summary(),
     }
+    if GT.get("acc") is not None and searcher is None:
+        from paper_1404_1831_b200 import evalbench
+
+        n = GT["n"]
+        nn, _ = GT["acc"].result()
+        r = evalbench.recall_at(res.ids[:n], res.counts[:n], nn)
+        line["recall"] = {**{f"R@{c}": v for c, v in r.items()}, "queries": n,
+                          "ground_truth": "exact NN of each sampled query over the whole base (int8 tensor-core "
+                                          "GEMM on x-128, exact distances; f64 for non-integer data), ties to the "
+                                          "smaller id (vecio.brute_force_knn)",
+                          "definition": "evalbench.recall_at: true NN among the first c returned ids"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline and host is not None:
         try:
             qnp = q.cpu().numpy()

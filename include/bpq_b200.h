@@ -229,6 +229,12 @@ int bpq_merge_topk(const float *dists, const uint32_t *ids, const int32_t *count
                    int64_t nq, int32_t k, float *out_dist, uint32_t *out_ids,
                    int32_t *out_count, void *stream);
 
+/* The same merge over the packed buffer of one all-gather: shard s occupies
+ * words [s * W, (s + 1) * W), W = 2 * nq * k + nq, laid out as dists f32
+ * [nq, k] | ids u32 [nq, k] | counts i32 [nq]. */
+int bpq_merge_topk_packed(const void *packed, int32_t g, int64_t nq, int32_t k, float *out_dist,
+                          uint32_t *out_ids, int32_t *out_count, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

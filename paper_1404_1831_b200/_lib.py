@@ -86,6 +86,7 @@ SIGNATURES = {
     "bpq_rotate": (ctypes.c_int, [P, I64, I32, P, P, P]),
     "bpq_coarse_dots": (ctypes.c_int, [P, P, I64, P, P, P]),
     "bpq_merge_topk": (ctypes.c_int, [P, P, P, I32, I64, I32, P, P, P, P]),
+    "bpq_merge_topk_packed": (ctypes.c_int, [P, I32, I64, I32, P, P, P, P]),
 }
 
 _lib = None

@@ -57,6 +57,7 @@ struct Index {
     // populated-cell lists (optional): row i -> columns j, column j -> rows i
     const uint32_t *rowptr, *colptr;
     const uint16_t *rowcols, *colrows;
+    int64_t populated;  // populated cells of the traversal table (row_ptr[T]; 0: unknown)
     std::vector<void *> owned;
 };
 

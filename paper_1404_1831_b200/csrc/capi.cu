@@ -160,6 +160,12 @@ extern "C" int bpq_index_create(const bpq_index_desc *d, int copy_from_host, bpq
         ix.bank1 = d->bank1;
         ix.bank2 = d->bank2;
         ix.rowptr = d->row_ptr;
+        ix.populated = 0;
+        if (d->row_ptr) {
+            uint32_t pc = 0;
+            if (cudaMemcpy(&pc, d->row_ptr + T, 4, cudaMemcpyDeviceToHost) == cudaSuccess) ix.populated = pc;
+            else cudaGetLastError();
+        }
         ix.rowcols = d->row_cols;
         ix.colptr = d->col_ptr;
         ix.colrows = d->col_rows;
@@ -194,6 +200,7 @@ extern "C" int bpq_index_create(const bpq_index_desc *d, int copy_from_host, bpq
             // the lists describe the traversal table (global_offsets when
             // sharded): size them by its populated count, row_ptr[T]
             const size_t P = std::max<size_t>(d->row_ptr[T], 1);
+            ix.populated = (int64_t)d->row_ptr[T];
             rc |= copy_in(d->row_ptr, T + 1, ix.owned, &ix.rowptr);
             rc |= copy_in(d->col_ptr, T + 1, ix.owned, &ix.colptr);
             rc |= copy_in(d->row_cols, P, ix.owned, &ix.rowcols);

@@ -200,9 +200,10 @@ __global__ void gather_rows_kernel(const uint32_t *__restrict__ order, int64_t n
 }
 
 // per query: G-way merge of sorted per-shard lists by (dist, id)
+// (shard s's lists start `stride` / `cstride` elements after shard s - 1's)
 __global__ void merge_kernel(const float *__restrict__ dists, const uint32_t *__restrict__ ids,
-                             const int32_t *__restrict__ counts, int g, int64_t nq, int k,
-                             float *__restrict__ od, uint32_t *__restrict__ oi,
+                             const int32_t *__restrict__ counts, int g, int64_t nq, int k, int64_t stride,
+                             int64_t cstride, float *__restrict__ od, uint32_t *__restrict__ oi,
                              int32_t *__restrict__ oc) {
     int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= nq) return;
@@ -211,7 +212,7 @@ __global__ void merge_kernel(const float *__restrict__ dists, const uint32_t *__
     int total = 0;
     for (int s = 0; s < g; s++) {
         pos[s] = 0;
-        int c = counts[(int64_t)s * nq + q];
+        int c = counts[(int64_t)s * cstride + q];
         cnt[s] = c < 0 ? 0 : c;
         total += cnt[s];
     }
@@ -222,7 +223,7 @@ __global__ void merge_kernel(const float *__restrict__ dists, const uint32_t *__
         uint32_t bi = 0;
         for (int s = 0; s < g; s++) {
             if (pos[s] >= cnt[s]) continue;
-            int64_t at = ((int64_t)s * nq + q) * k + pos[s];
+            int64_t at = (int64_t)s * stride + q * k + pos[s];
             float d = dists[at];
             uint32_t id = ids[at];
             if (bs < 0 || d < bd || (d == bd && id < bi)) {
@@ -393,7 +394,20 @@ extern "C" int bpq_merge_topk(const float *dists, const uint32_t *ids, const int
     BPQ_CHECK(g >= 1 && g <= 16 && k >= 1, BPQ_ERR_INVALID, "merge needs 1 <= shards <= 16, k >= 1");
     if (nq == 0) return BPQ_OK;
     bpq::merge_kernel<<<(unsigned)((nq + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
-        dists, ids, counts, g, nq, k, out_dist, out_ids, out_count);
+        dists, ids, counts, g, nq, k, nq * k, nq, out_dist, out_ids, out_count);
+    BPQ_CUDA_TRY(cudaGetLastError());
+    return BPQ_OK;
+}
+
+extern "C" int bpq_merge_topk_packed(const void *packed, int32_t g, int64_t nq, int32_t k, float *out_dist,
+                                     uint32_t *out_ids, int32_t *out_count, void *stream) {
+    BPQ_CHECK(g >= 1 && g <= 16 && k >= 1, BPQ_ERR_INVALID, "merge needs 1 <= shards <= 16, k >= 1");
+    if (nq == 0) return BPQ_OK;
+    const int64_t words = 2 * nq * k + nq;  // per shard: dists [nq, k] | ids [nq, k] | counts [nq]
+    const uint32_t *w = static_cast<const uint32_t *>(packed);
+    bpq::merge_kernel<<<(unsigned)((nq + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+        reinterpret_cast<const float *>(w), w + nq * k, reinterpret_cast<const int32_t *>(w + 2 * nq * k), g, nq, k,
+        words, words, out_dist, out_ids, out_count);
     BPQ_CUDA_TRY(cudaGetLastError());
     return BPQ_OK;
 }

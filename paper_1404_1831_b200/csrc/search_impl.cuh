@@ -468,6 +468,17 @@ __device__ __forceinline__ void rotate_code(const uint32_t (&w)[4], int rot, uin
     }
 }
 
+// Pairwise sum of the M step values, ((v0 + v1) + (v2 + v3)) + ..., fixed
+// structure (3 or 4 dependent adds instead of M - 1)
+template <int MT>
+__device__ __forceinline__ float tree_sum(float (&v)[MT]) {
+#pragma unroll
+    for (int w = 1; w < MT; w *= 2)
+#pragma unroll
+        for (int i = 0; i < MT; i += 2 * w) v[i] = __fadd_rn(v[i], v[i + w]);
+    return v[0];
+}
+
 // the same sum through the plain [p][c] fold table (small cells in the
 // traversal kernel): identical operation order, so an entry scores the same
 // bits whichever kernel scans it
@@ -477,32 +488,31 @@ __device__ __forceinline__ float dist_pt_plain(const float *tab, int K, int y, f
     const int x = y % MT;
     uint32_t r[4];
     rotate_code<MT>(w, x, r);
-    float s = 0.f;
+    float v[MT];
 #pragma unroll
     for (int i = 0; i < MT; i++) {
         const uint32_t c = __byte_perm(r[i >> 2], 0u, 0x4440u | (uint32_t)(i & 3));
-        const float v = tab[((x + i) & (MT - 1)) * K + (int)c];
-        s = i == 0 ? v : __fadd_rn(s, v);
+        v[i] = tab[((x + i) & (MT - 1)) * K + (int)c];
     }
-    const float acc = __fadd_rn(__fadd_rn(s, pt), cbase);
+    const float acc = __fadd_rn(__fadd_rn(tree_sum<MT>(v), pt), cbase);
     return acc < 0.f ? 0.f : acc;
 }
 
 // point-term FBPQ distance through the replicated fold table (M = 8 or 16):
-// the parts are summed in the lane's rotated order, then + pt + cell_base
+// the parts are summed in the lane's rotated order (pairwise), then + pt +
+// cell_base.  offb[i] = byte offset of the lane's slot for step i.
 template <int MT>
-__device__ __forceinline__ float dist_pt_rep(const float *tab, const LaneLut<MT> &L, float cbase, float pt,
+__device__ __forceinline__ float dist_pt_rep(const char *tabb, const int (&offb)[MT], int rot, float cbase, float pt,
                                              const uint32_t (&w)[4]) {
     uint32_t r[4];
-    rotate_code<MT>(w, L.rot, r);
-    float s = 0.f;
+    rotate_code<MT>(w, rot, r);
+    float v[MT];
 #pragma unroll
     for (int i = 0; i < MT; i++) {
         const uint32_t c = __byte_perm(r[i >> 2], 0u, 0x4440u | (uint32_t)(i & 3));
-        const float v = tab[(int)(c << 5) + L.off[i]];
-        s = i == 0 ? v : __fadd_rn(s, v);
+        v[i] = *reinterpret_cast<const float *>(tabb + (c << 7) + offb[i]);
     }
-    const float acc = __fadd_rn(__fadd_rn(s, pt), cbase);
+    const float acc = __fadd_rn(__fadd_rn(tree_sum<MT>(v), pt), cbase);
     return acc < 0.f ? 0.f : acc;
 }
 
@@ -1400,8 +1410,11 @@ struct Query {
     // cell of its codeword's line, filtered by the cell's sorted position.
     // Each thread takes a contiguous run of work units with kEnumBatch
     // cell-table reads in flight.  Returns the band's global entry count.
-    __device__ unsigned long long enumerate_band(const uint4 *seg, const uint32_t *segLine, int nseg,
-                                                 uint32_t swork, int4 *list) {
+    // Visit every populated cell of the band's segments: visit(ca, cb, lin,
+    // global count, local start, local count) returns the weight to add.
+    template <typename Visit>
+    __device__ unsigned long long visit_band(const uint4 *seg, const uint32_t *segLine, int nseg, uint32_t swork,
+                                             Visit visit) {
         unsigned long long wb = 0;
         const uint32_t per = (swork + NT - 1) / NT;
         uint32_t f = threadIdx.x * per;
@@ -1481,15 +1494,124 @@ struct Query {
                             lst = (uint32_t)g0[x];
                             lcn = (uint32_t)(g1[x] - g0[x]);
                         }
-                        uint32_t pos = atomicAdd(&S.nlist, 1u);
-                        list[pos] = make_int4((ca[x] << 16) | cbv[x], (int)(uint32_t)(g1[x] - g0[x]),
-                                              (int)lst, (int)lcn);
-                        wb += (unsigned long long)(g1[x] - g0[x]);
+                        wb += visit(ca[x], cbv[x], lin[x], (uint32_t)(g1[x] - g0[x]), lst, lcn);
                     }
                 }
             }
         }
         return block_sum_u64(S, wb);
+    }
+
+    // Append the band's populated cells to list (at most kBandCap: S.nlist
+    // counts them all, so the caller detects an overflow).
+    __device__ unsigned long long enumerate_band(const uint4 *seg, const uint32_t *segLine, int nseg,
+                                                 uint32_t swork, int4 *list) {
+        return visit_band(seg, segLine, nseg, swork,
+                          [&](int ca, int cb, unsigned long long, uint32_t gc, uint32_t lst, uint32_t lcn) {
+                              const uint32_t pos = atomicAdd(&S.nlist, 1u);
+                              if (pos < (uint32_t)kBandCap)
+                                  list[pos] = make_int4((ca << 16) | cb, (int)gc, (int)lst, (int)lcn);
+                              return (unsigned long long)gc;
+                          });
+    }
+
+    // A band holding more than kBandCap populated cells (a tie plateau: one
+    // key value shared by that many cells, which no key threshold can split)
+    // is taken in windows of the reference heap's full order (key, oi * T +
+    // oj): each window's upper bound is the kBandCap-th smallest composite key
+    // above the previous window, found by an MSB radix select whose digit
+    // histograms re-enumerate the band (12 passes over 8 key + 4 lin bytes).
+    // Returns true when the cutoff fell inside the band (query done), false
+    // when the whole band was scanned (W updated).
+    __device__ __noinline__ bool plateau_windows(const uint4 *seg, const uint32_t *segLine, int nseg, uint32_t swork,
+                                    int4 *listA, int4 *listB, unsigned long long &W, unsigned long long L) {
+        unsigned long long lo_k = 0;
+        uint32_t lo_l = 0;
+        bool have_lo = false;
+        auto above_lo = [&](unsigned long long kb, uint32_t ln) {
+            return !have_lo || kb > lo_k || (kb == lo_k && ln > lo_l);
+        };
+        for (;;) {
+            // kBandCap-th smallest composite key above lo, digit by digit
+            unsigned long long pk = 0, mk = 0;  // key-byte prefix / mask
+            uint32_t pl = 0, ml = 0;            // lin-byte prefix / mask
+            uint32_t rank = (uint32_t)kBandCap;
+            bool all = false;
+            for (int d = 0; d < 12; d++) {
+                for (int i = threadIdx.x; i < 256; i += NT) S.hist_c[i] = 0;
+                __syncthreads();
+                visit_band(seg, segLine, nseg, swork,
+                           [&](int ca, int cb, unsigned long long lin, uint32_t, uint32_t, uint32_t) {
+                               const unsigned long long kb = (unsigned long long)__double_as_longlong(key(ca, cb));
+                               const uint32_t ln = (uint32_t)lin;
+                               if (above_lo(kb, ln) && (kb & mk) == pk && (ln & ml) == pl) {
+                                   const int v = d < 8 ? (int)((kb >> (56 - 8 * d)) & 0xFF)
+                                                       : (int)((ln >> (24 - 8 * (d - 8))) & 0xFF);
+                                   atomicAdd(&S.hist_c[v], 1u);
+                               }
+                               return 0ull;
+                           });
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    uint32_t run = 0, tot = 0;
+                    for (int v = 0; v < 256; v++) tot += S.hist_c[v];
+                    S.sel_v = -1;
+                    if (d == 0 && tot <= rank) {
+                        S.sel_v = 256;  // everything left fits in one window
+                    } else {
+                        for (int v = 0; v < 256; v++) {
+                            if (run + S.hist_c[v] >= rank) {
+                                S.sel_v = v;
+                                S.tsel_below = run;
+                                break;
+                            }
+                            run += S.hist_c[v];
+                        }
+                    }
+                }
+                __syncthreads();
+                const int v = S.sel_v;
+                if (v == 256) {
+                    all = true;
+                    break;
+                }
+                rank -= (uint32_t)S.tsel_below;
+                if (d < 8) {
+                    pk |= (unsigned long long)v << (56 - 8 * d);
+                    mk |= 0xFFull << (56 - 8 * d);
+                } else {
+                    pl |= (uint32_t)v << (24 - 8 * (d - 8));
+                    ml |= 0xFFu << (24 - 8 * (d - 8));
+                }
+                __syncthreads();
+            }
+            // the window (lo, hi] into listA
+            if (threadIdx.x == 0) S.nlist = 0;
+            __syncthreads();
+            const unsigned long long wb = visit_band(
+                seg, segLine, nseg, swork,
+                [&](int ca, int cb, unsigned long long lin, uint32_t gc, uint32_t lst, uint32_t lcn) {
+                    const unsigned long long kb = (unsigned long long)__double_as_longlong(key(ca, cb));
+                    const uint32_t ln = (uint32_t)lin;
+                    if (!above_lo(kb, ln) || !(all || kb < pk || (kb == pk && ln <= pl))) return 0ull;
+                    const uint32_t pos = atomicAdd(&S.nlist, 1u);
+                    if (pos < (uint32_t)kBandCap) listA[pos] = make_int4((ca << 16) | cb, (int)gc, (int)lst, (int)lcn);
+                    return (unsigned long long)gc;
+                });
+            const int n = (int)min(S.nlist, (uint32_t)kBandCap);
+            if (W + wb < L) {
+                emit(listA, n, -1, 0);
+                W += wb;
+                if (all) return false;
+                lo_k = pk;
+                lo_l = pl;
+                have_lo = true;
+                __syncthreads();
+            } else {
+                final_select(listA, listB, n, L - W);
+                return true;
+            }
+        }
     }
 
     // ------------------------------------------------------------------
@@ -1903,12 +2025,8 @@ struct Query {
                         cHi = chi;
                     }
                 }
-                if (cHi - Cprev > (unsigned long long)kBandCap) {
-                    // a single key value shared by more than kBandCap cells
-                    if (threadIdx.x == 0) S.err = 1;
-                    __syncthreads();
-                    return;
-                }
+                // cHi - Cprev > kBandCap: a single key value shared by more than
+                // kBandCap cells; the populated ones are counted below
             }
             // new line boundaries at tauHi and the active line counts
             PROF(PH_BOUNDS);
@@ -1969,9 +2087,26 @@ struct Query {
             PROF(PH_ENUM);
             const unsigned long long wb = enumerate_band(seg, segLine, (int)nseg, swork, listA);
             const int n = (int)S.nlist;
-            if (W + wb < L) {
-                emit(listA, n, -1, 0);
-                W += wb;
+            bool consumed;
+            if (n > kBandCap) {
+                // tie plateau: more populated cells than one band holds
+                if (plateau_windows(seg, segLine, (int)nseg, swork, listA, listB, W, L)) {
+                    if (A.out_popped) {
+                        __syncthreads();
+                        popped = count_le(__longlong_as_double((long long)S.cut_key), rowB, RA, colB, CA,
+                                          nullptr, nullptr);
+                    }
+                    break;
+                }
+                consumed = true;
+            } else {
+                consumed = W + wb < L;
+                if (consumed) {
+                    emit(listA, n, -1, 0);
+                    W += wb;
+                }
+            }
+            if (consumed) {
                 Cprev = cHi;
                 for (int a = threadIdx.x; a < nR; a += NT) rowB[a] = rowNew[a];
                 for (int b = threadIdx.x; b < nC; b += NT) colB[b] = colNew[b];
@@ -2154,7 +2289,17 @@ __global__ void __launch_bounds__(NT, 2) big_scan_kernel(Args<KT, OffT> A) {
     float *stp = reinterpret_cast<float *>(stc + (size_t)kRingS * kCh * MT);  // [kRingS][kCh] point terms
     const int K = A.K, k = A.k;
     const uint32_t nal = A.n_local & ~3u;  // 4-aligned end of the arrays
-    const LaneLut<MT> L((int)(threadIdx.x & 31));
+    // this lane's rotation and replica slots (chunks start at a 32-entry boundary: lane l scores
+    // entries with index % 32 == l); byte offsets into the replicated table
+    const char *tabb = reinterpret_cast<const char *>(tab);
+    int offb[MT];
+    int rot;
+    {
+        const LaneLut<MT> L((int)(threadIdx.x & 31));
+        rot = L.rot;
+#pragma unroll
+        for (int i = 0; i < MT; i++) offb[i] = L.off[i] * 4;
+    }
     if (threadIdx.x == 0) {
         for (int st = 0; st < kRingS; st++) mbar_init(&S.mbar[st], 1);
         mbar_fence_init();
@@ -2236,32 +2381,42 @@ __global__ void __launch_bounds__(NT, 2) big_scan_kernel(Args<KT, OffT> A) {
             const float cb = __int_as_float(cl.z);
             const uint32_t b1 = min(min(c_c + (uint32_t)kCh, (end + 3u) & ~3u), nal);
             const uint32_t thr_hi = (uint32_t)(S.thr >> 32);
+            // straight-line over the thread's kPer entries (independent chains): codes and point
+            // terms from the stage (stale slots past the copied range are masked below), the rare
+            // entries past the arrays' aligned end from global memory
+            uint32_t w[kPer][4];
+            float ptv[kPer], acc[kPer];
 #pragma unroll
             for (int u = 0; u < kPer; u++) {
                 const int j = u * NT + threadIdx.x;
-                const uint32_t e = c_c + j;
-                if (e >= lst && e < end) {
-                    uint32_t w[4];
-                    float ptv;
-                    if (e < b1) {
-                        if constexpr (MT == 16) {
-                            const uint4 v = *reinterpret_cast<const uint4 *>(stc + ((size_t)slot * kCh + j) * MT);
-                            w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
-                        } else {
-                            const uint2 v = *reinterpret_cast<const uint2 *>(stc + ((size_t)slot * kCh + j) * MT);
-                            w[0] = v.x; w[1] = v.y; w[2] = 0; w[3] = 0;
-                        }
-                        ptv = stp[slot * kCh + j];
-                    } else {  // past the aligned end of the arrays
-                        load_code<MT>(A.codes + (size_t)e * MT, w, MT);
-                        ptv = __ldg(A.pterm + e);
+                if constexpr (MT == 16) {
+                    const uint4 v = *reinterpret_cast<const uint4 *>(stc + ((size_t)slot * kCh + j) * MT);
+                    w[u][0] = v.x; w[u][1] = v.y; w[u][2] = v.z; w[u][3] = v.w;
+                } else {
+                    const uint2 v = *reinterpret_cast<const uint2 *>(stc + ((size_t)slot * kCh + j) * MT);
+                    w[u][0] = v.x; w[u][1] = v.y; w[u][2] = 0; w[u][3] = 0;
+                }
+                ptv[u] = stp[slot * kCh + j];
+            }
+            if (c_c + (uint32_t)kCh > b1 && end > b1) {
+#pragma unroll
+                for (int u = 0; u < kPer; u++) {
+                    const uint32_t e = c_c + u * NT + threadIdx.x;
+                    if (e >= b1 && e < end) {
+                        load_code<MT>(A.codes + (size_t)e * MT, w[u], MT);
+                        ptv[u] = __ldg(A.pterm + e);
                     }
-                    const float acc = dist_pt_rep<MT>(tab, L, cb, ptv, w);
-                    const uint32_t db = canon_bits(acc);
-                    if (db <= thr_hi) {
-                        const unsigned long long kk = ((unsigned long long)db << 32) | __ldg(A.ids + e);
-                        if (kk < S.thr) tk[atomicAdd(&S.ntk, 1u)] = kk;
-                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kPer; u++) acc[u] = dist_pt_rep<MT>(tabb, offb, rot, cb, ptv[u], w[u]);
+#pragma unroll
+            for (int u = 0; u < kPer; u++) {
+                const uint32_t e = c_c + u * NT + threadIdx.x;
+                const uint32_t db = canon_bits(acc[u]);
+                if (e >= lst && e < end && db <= thr_hi) {
+                    const unsigned long long kk = ((unsigned long long)db << 32) | __ldg(A.ids + e);
+                    if (kk < S.thr) tk[atomicAdd(&S.ntk, 1u)] = kk;
                 }
             }
             c_c += kCh;
@@ -2345,9 +2500,17 @@ void fill_args(Args<float, uint32_t> &A, const Index &ix, const float *queries, 
     A.cross2 = ix.cross2;
     A.pterm = ENGINE == BPQ_ENGINE_FBPQ ? ix.pterm : nullptr;
     A.lut_min = effective_lut_min();
-    static const int nb0_env = getenv("BPQ_NB0") ? atoi(getenv("BPQ_NB0")) : 0;  // A/B experiments
+    const int nb0_env = getenv("BPQ_NB0") ? atoi(getenv("BPQ_NB0")) : 0;  // A/B experiments (read per launch)
     // first sparse-traversal batch: small budgets stop within a few lines
-    A.nb0 = nb0_env > 0 ? (nb0_env < NT ? nb0_env : NT) : budget <= 2000 ? 32 : budget <= 5000 ? 64 : 128;
+    // first sparse-traversal batch: about 6x the populated cells the budget needs (the budget over the
+    // mean entries per populated cell), 16..256 lines; without a populated count, by budget alone
+    int nb0 = budget <= 2000 ? 32 : budget <= 5000 ? 64 : 128;
+    if (ix.populated > 0 && ix.N_global > 0) {
+        const double cells = (double)budget * (double)ix.populated / (double)ix.N_global;
+        nb0 = 16;
+        while (nb0 < NT && nb0 < 6.0 * cells) nb0 *= 2;
+    }
+    A.nb0 = nb0_env > 0 ? (nb0_env < NT ? nb0_env : NT) : nb0;
     A.bank1 = ix.bank1;
     A.bank2 = ix.bank2;
     A.rot1 = ix.rot1;
@@ -2447,7 +2610,7 @@ int launch_big_one(const Index &ix, const float *queries, int64_t q0, int64_t nq
         fill_args<BPQ_ENGINE_FBPQ, MT>(A, ix, queries, q0, nq, budget, k, ws, out_dist, out_ids, out_count,
                                        nullptr, nullptr);
         if (A.big_cells == nullptr) return BPQ_OK;
-        A.tkcap = ((k + 255) & ~255) + ring_chunk<MT>();
+        A.tkcap = ((k + 255) & ~255) + 2 * ring_chunk<MT>();  // compaction once per >= one chunk of offers
         A.tk_off = (int)((sizeof(Smem) + (size_t)32 * ix.K * 4 + 15) & ~(size_t)15);
         const size_t smem = (size_t)A.tk_off + (size_t)A.tkcap * 8 + ring_bytes<MT>();
         auto kfn = big_scan_kernel<MT, float, uint32_t>;

@@ -70,6 +70,43 @@ def merge_results(dists, ids, counts, k: int, stream=None) -> SearchResult:
     return out
 
 
+def pack_lists(dists, ids, counts):
+    """One rank's [nq, k] dists / ids and [nq] counts as the 32-bit word
+    buffer of the all-gather: dists | ids | counts (2 nq k + nq words)."""
+    import torch
+
+    nq, k = dists.shape
+    buf = torch.empty(2 * nq * k + nq, dtype=torch.int32, device=dists.device)
+    buf[: nq * k].copy_(dists.reshape(-1).view(torch.int32))
+    buf[nq * k: 2 * nq * k].copy_(ids.reshape(-1).view(torch.int32))
+    buf[2 * nq * k:].copy_(counts.view(torch.int32))
+    return buf
+
+
+def unpack_lists(gathered, g: int, nq: int, k: int):
+    """Host view of an all-gathered packed buffer: (dists [g, nq, k] f32,
+    ids [g, nq, k] u32, counts [g, nq] i32) numpy arrays."""
+    w = np.asarray(gathered.cpu() if hasattr(gathered, "cpu") else gathered).view(np.int32).reshape(g, -1)
+    d = w[:, : nq * k].view(np.float32).reshape(g, nq, k)
+    i = w[:, nq * k: 2 * nq * k].view(np.uint32).reshape(g, nq, k)
+    c = w[:, 2 * nq * k:].reshape(g, nq)
+    return d, i, c
+
+
+def merge_packed(gathered, g: int, nq: int, k: int, stream=None) -> SearchResult:
+    """Merge the all-gathered packed buffer [g][dists nq*k | ids nq*k |
+    counts nq] (32-bit words) on the device."""
+    import torch
+
+    out = SearchResult(torch.empty((nq, k), dtype=torch.float32, device=gathered.device),
+                       torch.empty((nq, k), dtype=torch.int32, device=gathered.device),
+                       torch.empty((nq,), dtype=torch.int32, device=gathered.device))
+    lib = _lib.load()
+    _lib.check(lib.bpq_merge_topk_packed(_lib.ptr(gathered), g, nq, k, _lib.ptr(out.dists), _lib.ptr(out.ids),
+                                         _lib.ptr(out.counts), _lib.stream_ptr(stream)), "merge_topk_packed")
+    return out
+
+
 def merge_results_host(dists, ids, counts, k: int):
     """Host restatement of the merge used by CPU (gloo) tests of the
     distributed plumbing; the product path uses merge_results."""
@@ -109,10 +146,8 @@ class ShardedSearcher:
         if world == 1 and not self.force_collective:
             return res
         nq = res.dists.shape[0]
-        gd = torch.empty((world, nq, k), dtype=torch.float32, device=res.dists.device)
-        gi = torch.empty((world, nq, k), dtype=torch.int32, device=res.dists.device)
-        gc = torch.empty((world, nq), dtype=torch.int32, device=res.dists.device)
-        dist.all_gather_into_tensor(gd, res.dists, group=self.group)
-        dist.all_gather_into_tensor(gi, res.ids, group=self.group)
-        dist.all_gather_into_tensor(gc, res.counts, group=self.group)
-        return merge_results(gd, gi, gc, k)
+        # one all-gather of a packed [dists | ids | counts] buffer per rank
+        mine = pack_lists(res.dists, res.ids, res.counts)
+        gathered = torch.empty(world * mine.numel(), dtype=torch.int32, device=mine.device)
+        dist.all_gather_into_tensor(gathered, mine, group=self.group)
+        return merge_packed(gathered, world, nq, k)

@@ -656,3 +656,40 @@ def test_nearest_centroids_tensor_cores_vs_f64(torch_cuda, nc, kind):
     assert np.all(got - best <= 1e-6 * scale), np.max((got - best) / scale)
     want_d2 = np.maximum(best + (x.astype(np.float64) ** 2).sum(1), 0)
     assert np.all(np.abs(d2 - want_d2) <= 1e-4 * np.maximum(want_d2, 1e-3) + 1e-6 * scale)
+
+
+@pytest.mark.parametrize("L", [1000, 30_000, 36_000])
+def test_tie_plateau_every_key_ties(torch_cuda, oracle, L):
+    """Every cell has the same key: 192 coarse codewords per half at +-10 e_u
+    and the query at the origin give r = 100 for all of them, and one point
+    per cell fills all 36,864 cells.  The reference heap then pops cells in
+    (oi, oj) order (numba_backend.py:28-144), which the band traversal must
+    reproduce through the plateau windows (more populated cells than one
+    band holds).  L = 36,000 needs two windows."""
+    from paper_1404_1831_b200 import DeviceIndex
+
+    rng = np.random.default_rng(5)
+    dh, t, m, kk = 96, 192, 8, 16
+    cb = np.zeros((t, dh), np.float32)
+    for i in range(t):
+        cb[i, i // 2] = 10.0 if i % 2 == 0 else -10.0
+    ii, jj = np.meshgrid(np.arange(t), np.arange(t), indexing="ij")
+    base = np.concatenate([cb[ii.ravel()], cb[jj.ravel()]], 1)
+    base += rng.normal(scale=0.01, size=base.shape).astype(np.float32)
+    books = (0.01 * rng.normal(size=(m, kk, 2 * dh // m))).astype(np.float32)
+    off, ids, codes = oracle.build_index(base, cb, cb, books)
+    assert np.all(np.diff(off) == 1)
+    idx = oracle.Index(cb, cb, off, ids, codes, books=books)
+    # exact mode: candidate distances bit-identical to the oracle, so equal-distance ties break the same way
+    dix = DeviceIndex(c1=cb, c2=cb, offsets=off, ids=ids, codes=codes, books=books, tables=idx.tables, exact=True)
+    q = np.zeros((2, 2 * dh), np.float32)
+    for eng in ("fbpq", "baseline"):
+        wd, wi, wc, _ = oracle.search_batch_numpy(idx, eng, q, L, 50)
+        d, i, c = dix.search(q, L, 50, eng).numpy()
+        assert (c >= 0).all(), "tie plateau reported as failure"
+        # every key ties, so the boundary near-tie rule would excuse any candidate set: demand the
+        # reference's exact set (the first L cells in (oi, oj) order)
+        np.testing.assert_array_equal(c, wc)
+        for x in range(q.shape[0]):
+            assert set(i[x, : c[x]].view(np.uint32).tolist()) == set(wi[x, : wc[x]].tolist())
+        check_topk(d, i, c, wd, wi, wc, _qn(q))

@@ -58,17 +58,13 @@ def _worker(rank, world, port, c0, q, L, k, out_path):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     shard = sharded.split_index_arrays(c0["offsets"], c0["ids"], c0["codes"], world)[rank]
     d, i, c = _local_search(c0, shard, q, L, k)
-    td = torch.from_numpy(d)
-    ti = torch.from_numpy(i.view(np.int32))
-    tc = torch.from_numpy(c)
-    gd = [torch.empty_like(td) for _ in range(world)]
-    gi = [torch.empty_like(ti) for _ in range(world)]
-    gc = [torch.empty_like(tc) for _ in range(world)]
-    dist.all_gather(gd, td)
-    dist.all_gather(gi, ti)
-    dist.all_gather(gc, tc)
-    md, mi, mc = sharded.merge_results_host(torch.stack(gd).numpy(), torch.stack(gi).numpy(),
-                                            torch.stack(gc).numpy(), k)
+    # the exchange of ShardedSearcher.search: one all-gather of the packed
+    # [dists | ids | counts] buffer (gloo has no all_gather_into_tensor)
+    mine = sharded.pack_lists(torch.from_numpy(d), torch.from_numpy(i.view(np.int32)), torch.from_numpy(c))
+    parts = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(parts, mine)
+    gd, gi, gc = sharded.unpack_lists(torch.cat(parts), world, q.shape[0], k)
+    md, mi, mc = sharded.merge_results_host(gd, gi, gc, k)
     if rank == 0:
         np.savez(out_path, d=md, i=mi, c=mc)
     dist.barrier()
