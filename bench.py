@@ -524,10 +524,14 @@ def main():
         torch.cuda.synchronize()
         _lib.load().bpq_debug_set_phase_buffer(None)
         names = ["prologue", "tau_search|sparse_reclassify", "band_bounds|sparse_activate", "enumerate|sparse_gather",
-                 "scan", "lut_scan", "topk_compact", "final_select", "finish", "idle", "extend_prefix"]
-        c = ctr.cpu().numpy()[:11].astype(float)
+                 "scan", "lut_scan", "topk_compact", "final_select", "finish", "idle", "extend_prefix",
+                 "stream_prologue", "stream_wait", "stream_score", "stream_compact", "stream_finish"]
+        c = ctr.cpu().numpy()[:16].astype(float)
+        k1, k2 = c[:11], c[11:16]
         log(json.dumps({"phase_profile_compiled": bool(on),
-                        "phase_share": {n: round(float(v / max(c.sum(), 1)), 4) for n, v in zip(names, c)}}))
+                        "traversal_kernel_share": {n: round(float(v / max(k1.sum(), 1)), 4) for n, v in zip(names, k1)},
+                        "stream_kernel_share": {n: round(float(v / max(k2.sum(), 1)), 4)
+                                                for n, v in zip(names[11:], k2)}}))
     for _ in range(args.warmup):
         dix.search(q, L, k, engine, out=out, workspace=ws)
     torch.cuda.synchronize()

@@ -191,7 +191,9 @@ __device__ __forceinline__ int prof_nop() { return 0; }
 
 // Optional per-phase cycle accounting (compile with -DBPQ_PHASE_PROF): thread 0
 // of each CTA attributes elapsed clock64 cycles to the current phase.
-enum Phase { PH_PROLOGUE, PH_TAU, PH_BOUNDS, PH_ENUM, PH_SCAN, PH_LUT, PH_COMPACT, PH_FINAL, PH_FINISH, PH_IDLE, PH_EXTEND, PH_N };
+// (PH_B*: the large-cell stream kernel)
+enum Phase { PH_PROLOGUE, PH_TAU, PH_BOUNDS, PH_ENUM, PH_SCAN, PH_LUT, PH_COMPACT, PH_FINAL, PH_FINISH, PH_IDLE, PH_EXTEND,
+             PH_BPRO, PH_BWAIT, PH_BSCORE, PH_BCOMPACT, PH_BFIN, PH_N };
 
 template <typename KT, typename OffT>
 struct Args {
@@ -2303,16 +2305,24 @@ __global__ void __launch_bounds__(NT, 2) big_scan_kernel(Args<KT, OffT> A) {
     if (threadIdx.x == 0) {
         for (int st = 0; st < kRingS; st++) mbar_init(&S.mbar[st], 1);
         mbar_fence_init();
+#ifdef BPQ_PHASE_PROF
+        S.prof_ph = PH_IDLE;
+        S.prof_t = clock64();
+#endif
     }
     uint32_t ph = 0;  // stage mbarrier parities (block-uniform)
     for (;;) {
+        PROF(PH_BPRO);
         if (threadIdx.x == 0) {
             const unsigned int c = atomicAdd(A.counter, 1u);
             S.qidx = c < *A.bigq_count ? (int64_t)A.bigq_list[c] : (int64_t)-1;
         }
         __syncthreads();
         const int64_t qi = S.qidx;
-        if (qi < 0) return;
+        if (qi < 0) {
+            PROF(PH_IDLE);
+            return;
+        }
         // replicated fold table and the small cells' top-k
         const float *fq = A.fold + (size_t)qi * MT * K;
         for (int x = threadIdx.x; x < MT * K; x += NT) {
@@ -2374,8 +2384,10 @@ __global__ void __launch_bounds__(NT, 2) big_scan_kernel(Args<KT, OffT> A) {
         for (int r = 0; x_c < nb; r++) {
             issue((r + kRingS - 1) % kRingS);
             const int slot = r % kRingS;
+            PROF(PH_BWAIT);
             mbar_wait(&S.mbar[slot], (ph >> slot) & 1u);
             ph ^= 1u << slot;
+            PROF(PH_BSCORE);
             const int4 cl = __ldg(&cells[x_c]);
             const uint32_t lst = (uint32_t)cl.x, end = lst + (uint32_t)cl.y;
             const float cb = __int_as_float(cl.z);
@@ -2425,8 +2437,12 @@ __global__ void __launch_bounds__(NT, 2) big_scan_kernel(Args<KT, OffT> A) {
                 if (x_c < nb) c_c = (uint32_t)__ldg(&cells[x_c].x) & ~31u;
             }
             __syncthreads();
-            if (S.ntk > (uint32_t)(A.tkcap - kCh)) topk_compact(S, tk, k);
+            if (S.ntk > (uint32_t)(A.tkcap - kCh)) {
+                PROF(PH_BCOMPACT);
+                topk_compact(S, tk, k);
+            }
         }
+        PROF(PH_BFIN);
         topk_compact(S, tk, k);
         const int64_t qo = A.q0 + qi;
         write_topk(S, tk, k, A.ncand_q[qi], A.out_d + qo * k, A.out_ids + qo * k, A.out_count + qo);
