@@ -48,6 +48,7 @@ def log(*a):
 # resident (c1/c2) or streamed (c3/c4) during setup; reported as Recall@{1,10,100} (untimed)
 RECALL_Q = 1000
 GT = {}
+PROFILE = {}  # --phase-profile results, copied into the JSON line
 
 
 def _gt_start(q):
@@ -518,20 +519,30 @@ def main():
     if args.phase_profile:
         from paper_1404_1831_b200 import _lib
 
-        ctr = torch.zeros(16, dtype=torch.int64, device=device)
+        ctr = torch.zeros(32, dtype=torch.int64, device=device)
         on = _lib.load().bpq_debug_set_phase_buffer(_lib.ptr(ctr))
         dix.search(q, L, k, engine, out=out, workspace=ws)
         torch.cuda.synchronize()
         _lib.load().bpq_debug_set_phase_buffer(None)
         names = ["prologue", "tau_search|sparse_reclassify", "band_bounds|sparse_activate", "enumerate|sparse_gather",
                  "scan", "lut_scan", "topk_compact", "final_select", "finish", "idle", "extend_prefix",
-                 "stream_prologue", "stream_wait", "stream_score", "stream_compact", "stream_finish"]
-        c = ctr.cpu().numpy()[:16].astype(float)
-        k1, k2 = c[:11], c[11:16]
-        log(json.dumps({"phase_profile_compiled": bool(on),
-                        "traversal_kernel_share": {n: round(float(v / max(k1.sum(), 1)), 4) for n, v in zip(names, k1)},
-                        "stream_kernel_share": {n: round(float(v / max(k2.sum(), 1)), 4)
-                                                for n, v in zip(names[11:], k2)}}))
+                 "stream_prologue", "stream_wait", "stream_score", "stream_compact", "stream_finish",
+                 "residual_table_build"]
+        cc = ctr.cpu().numpy()
+        c = cc[:17].astype(float)
+        k1, k2 = np.concatenate([c[:11], c[16:17]]), c[11:16]
+        halves = int(cc[17])
+        prof = {"phase_profile_compiled": bool(on),
+                "traversal_kernel_share": {n: round(float(v / max(k1.sum(), 1)), 4)
+                                           for n, v in zip(names[:11] + names[16:17], k1)},
+                "stream_kernel_share": {n: round(float(v / max(k2.sum(), 1)), 4) for n, v in zip(names[11:16], k2)}}
+        if engine in ("hbpq", "baseline"):
+            # BASELINE configs[2] / SURVEY 8(d) d2: the local-table cost beside the scan
+            tb = dix.m // 2 * dix.k * (dix.dim // dix.m) * 4
+            prof["residual_tables"] = {"halves_built_per_batch": halves, "bytes_per_half": tb,
+                                       "bytes_per_batch": halves * tb, "halves_per_query": halves / nq}
+        log(json.dumps(prof))
+        PROFILE.update(prof)
     for _ in range(args.warmup):
         dix.search(q, L, k, engine, out=out, workspace=ws)
     torch.cuda.synchronize()
@@ -641,6 +652,8 @@ def main():
         "gpu_launches": (launches_per_step(dix, engine) + (1 if searcher is not None else 0)) * args.steps,
         "clocks": clk.summary(),
     }
+    if PROFILE:
+        line["phase_profile"] = PROFILE
     if GT.get("acc") is not None and searcher is None:
         from paper_1404_1831_b200 import evalbench
 

@@ -172,7 +172,8 @@ struct __align__(16) Smem {
 };
 
 #ifdef BPQ_PHASE_PROF
-__device__ __forceinline__ int prof_switch(Smem &S, unsigned long long *acc, int ph) {
+template <typename SM>
+__device__ __forceinline__ int prof_switch(SM &S, unsigned long long *acc, int ph) {
     int prev = S.prof_ph;
     __syncwarp();
     if (threadIdx.x == 0 && acc) {
@@ -193,7 +194,9 @@ __device__ __forceinline__ int prof_nop() { return 0; }
 // of each CTA attributes elapsed clock64 cycles to the current phase.
 // (PH_B*: the large-cell stream kernel)
 enum Phase { PH_PROLOGUE, PH_TAU, PH_BOUNDS, PH_ENUM, PH_SCAN, PH_LUT, PH_COMPACT, PH_FINAL, PH_FINISH, PH_IDLE, PH_EXTEND,
-             PH_BPRO, PH_BWAIT, PH_BSCORE, PH_BCOMPACT, PH_BFIN, PH_N };
+             PH_BPRO, PH_BWAIT, PH_BSCORE, PH_BCOMPACT, PH_BFIN, PH_LUTBUILD, PH_N };
+// counter slots after the phase cycles (phase-profiling builds): residual-table halves built
+constexpr int PROF_LUT_HALVES = PH_N;
 
 template <typename KT, typename OffT>
 struct Args {
@@ -282,7 +285,8 @@ __device__ __forceinline__ float block_sum_f32_ordered(Smem &S, float v) {
 }
 
 // exclusive scan of one u32 per thread; returns exclusive prefix, *total = sum
-__device__ __forceinline__ uint32_t block_excl_scan(Smem &S, uint32_t v, uint32_t *total) {
+template <typename SM>
+__device__ __forceinline__ uint32_t block_excl_scan(SM &S, uint32_t v, uint32_t *total) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     uint32_t x = v;
 #pragma unroll
@@ -304,10 +308,11 @@ __device__ __forceinline__ uint32_t block_excl_scan(Smem &S, uint32_t v, uint32_
     return off + x - v;
 }
 
+template <int BT = NT>
 __device__ __forceinline__ void bitonic_sort_u64(unsigned long long *a, int n) {
     for (int k = 2; k <= n; k <<= 1) {
         for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = threadIdx.x; i < n; i += NT) {
+            for (int i = threadIdx.x; i < n; i += BT) {
                 int ixj = i ^ j;
                 if (ixj > i) {
                     bool up = (i & k) == 0;
@@ -528,7 +533,10 @@ __device__ __forceinline__ float dist_recon(const Args<KT, OffT> &A, const float
     const int M2 = M / 2;
     const int K = A.K, ds = A.ds, dh = A.dh;
     float acc = 0.f;
-#pragma unroll
+    // M = 16: a rolled part loop (the fully unrolled 16-part reconstruction, times the
+    // emit loop's 4 candidates, made these instantiations take ~15 minutes in ptxas)
+    constexpr int kPartUnroll = MT == 16 ? 1 : 8;
+#pragma unroll kPartUnroll
     for (int p = 0; p < M; p++) {
         const int hp = p < M2 ? p : p - M2;
         const int row = p < M2 ? oi : oj;
@@ -573,13 +581,14 @@ __device__ __forceinline__ float dist_recon(const Args<KT, OffT> &A, const float
 // is in the low word).  An MSB-first radix select on the 64-bit keys finds
 // the k-th smallest in a few 256-bin histogram passes, then the survivors
 // are compacted to the front and the admission threshold becomes that key.
-__device__ void topk_compact(Smem &S, unsigned long long *__restrict__ tk, int k) {
+template <int BT = NT, typename SM>
+__device__ void topk_compact(SM &S, unsigned long long *__restrict__ tk, int k) {
     const uint32_t n = S.ntk;
     if ((int)n <= k) return;
     // bits shared by every buffered key (AND == OR) need no histogram pass:
     // start at the digit holding the highest differing bit
     unsigned long long ka = ~0ull, ko = 0ull;
-    for (uint32_t i = threadIdx.x; i < n; i += NT) {
+    for (uint32_t i = threadIdx.x; i < n; i += BT) {
         ka &= tk[i];
         ko |= tk[i];
     }
@@ -597,7 +606,7 @@ __device__ void topk_compact(Smem &S, unsigned long long *__restrict__ tk, int k
     ka = ~0ull;
     ko = 0ull;
 #pragma unroll
-    for (int w = 0; w < NW; w++) {
+    for (int w = 0; w < BT / 32; w++) {
         ka &= S.red[w];
         ko |= S.tor[w];
     }
@@ -607,9 +616,9 @@ __device__ void topk_compact(Smem &S, unsigned long long *__restrict__ tk, int k
     unsigned long long prefix = ka & pmask;
     uint32_t rank = (uint32_t)k;  // 1-based rank of the wanted key among matches
     for (int shift = top; shift >= 0; shift -= 8) {
-        for (int i = threadIdx.x; i < 256; i += NT) S.hist_c[i] = 0;
+        for (int i = threadIdx.x; i < 256; i += BT) S.hist_c[i] = 0;
         __syncthreads();
-        for (uint32_t i = threadIdx.x; i < n; i += NT) {
+        for (uint32_t i = threadIdx.x; i < n; i += BT) {
             const unsigned long long key = tk[i];
             if ((key & pmask) == prefix) atomicAdd(&S.hist_c[(key >> shift) & 0xFF], 1u);
         }
@@ -647,7 +656,7 @@ __device__ void topk_compact(Smem &S, unsigned long long *__restrict__ tk, int k
         pmask |= 0xFFull << shift;
         if (S.tcnt == 1u) {
             // a single key carries this prefix: it is the k-th smallest
-            for (uint32_t i = threadIdx.x; i < n; i += NT)
+            for (uint32_t i = threadIdx.x; i < n; i += BT)
                 if ((tk[i] & pmask) == prefix) S.tkey = tk[i];
             __syncthreads();
             prefix = S.tkey;
@@ -663,10 +672,10 @@ __device__ void topk_compact(Smem &S, unsigned long long *__restrict__ tk, int k
         S.nholes = 0;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < k; i += NT)
+    for (int i = threadIdx.x; i < k; i += BT)
         if (tk[i] > kth) S.holes[atomicAdd(&S.nholes, 1u)] = (uint16_t)i;
     __syncthreads();
-    for (uint32_t i = k + threadIdx.x; i < n; i += NT) {
+    for (uint32_t i = k + threadIdx.x; i < n; i += BT) {
         const unsigned long long key = tk[i];
         if (key <= kth) tk[S.holes[atomicAdd(&S.tcnt, 1u)]] = key;
     }
@@ -680,13 +689,14 @@ __device__ void topk_compact(Smem &S, unsigned long long *__restrict__ tk, int k
 
 // Write the compacted top-k (S.ntk <= k unique keys in tk) as select_top's
 // (dist asc, id asc) list of min(k, ncand) entries, padded with (+inf, ~0).
-__device__ void write_topk(Smem &S, unsigned long long *__restrict__ tk, int k, unsigned long long ncand,
+template <int BT = NT, typename SM>
+__device__ void write_topk(SM &S, unsigned long long *__restrict__ tk, int k, unsigned long long ncand,
                            float *__restrict__ od, uint32_t *__restrict__ oi, int32_t *__restrict__ oc) {
     const uint32_t n = S.ntk;
     const int cnt = (int)min((unsigned long long)k, ncand);
     if (n <= 512) {
         // keys are unique: each key's rank is its output position
-        for (int x = threadIdx.x; x < (int)n; x += NT) {
+        for (int x = threadIdx.x; x < (int)n; x += BT) {
             const unsigned long long kx = tk[x];
             int rank = 0;
             for (uint32_t y = 0; y < n; y++) rank += tk[y] < kx ? 1 : 0;
@@ -696,17 +706,17 @@ __device__ void write_topk(Smem &S, unsigned long long *__restrict__ tk, int k, 
     } else {
         int P2 = 1;
         while (P2 < (int)n) P2 <<= 1;
-        for (int i = threadIdx.x; i < P2; i += NT)
+        for (int i = threadIdx.x; i < P2; i += BT)
             if (i >= (int)n) tk[i] = ~0ull;
         __syncthreads();
-        bitonic_sort_u64(tk, P2);
-        for (int x = threadIdx.x; x < cnt; x += NT) {
+        bitonic_sort_u64<BT>(tk, P2);
+        for (int x = threadIdx.x; x < cnt; x += BT) {
             const unsigned long long kk = tk[x];
             od[x] = __uint_as_float((uint32_t)(kk >> 32));
             oi[x] = (uint32_t)kk;
         }
     }
-    for (int x = cnt + threadIdx.x; x < k; x += NT) {
+    for (int x = cnt + threadIdx.x; x < k; x += BT) {
         od[x] = INFINITY;
         oi[x] = 0xFFFFFFFFu;
     }
@@ -944,6 +954,10 @@ struct Query {
         const int lo_idx = oi == lut_i ? M2 * K : 0;
         const int hi_idx = oj == lut_j ? M2 * K : M * K;
         if (lo_idx < hi_idx) {
+            PROF(PH_LUTBUILD);
+#ifdef BPQ_PHASE_PROF
+            if (threadIdx.x == 0 && A.prof) atomicAdd(A.prof + PROF_LUT_HALVES, (unsigned long long)((hi_idx - lo_idx) / (M2 * K)));
+#endif
             for (int idx = lo_idx + threadIdx.x; idx < hi_idx; idx += NT) {
                 const int p = idx / K, c = idx - p * K;
                 const int hp = p < M2 ? p : p - M2;
@@ -977,6 +991,7 @@ struct Query {
                 lut[idx] = acc;
             }
             __syncthreads();
+            PROF(PH_LUT);
         }
         lut_i = oi;
         lut_j = oj;
@@ -2277,15 +2292,35 @@ constexpr int kRingS = BPQ_RING_S;
 template <int MT>
 __host__ __device__ constexpr int ring_bytes() { return kRingS * ring_chunk<MT>() * (MT + 4); }
 
-template <int MT, typename KT, typename OffT>
-__global__ void __launch_bounds__(NT, 2) big_scan_kernel(Args<KT, OffT> A) {
+// shared state of big_scan_kernel with BT threads
+template <int BT>
+struct __align__(16) ScanSmem {
+    unsigned long long mbar[kRingS];
+    uint32_t hist_c[256];
+    unsigned long long red[BT / 32];
+    unsigned long long tor[BT / 32];
+    unsigned long long thr;
+    uint32_t ntk;
+    int tsel_v;
+    uint32_t tcnt;
+    unsigned long long tsel_below;
+    unsigned long long tkey;
+    uint32_t nholes;
+    uint16_t holes[kMaxK];
+    int64_t qidx;
+    int prof_ph;
+    long long prof_t;
+};
+
+template <int MT, int BT, typename KT, typename OffT>
+__global__ void __launch_bounds__(BT, 2) big_scan_kernel(Args<KT, OffT> A) {
     static_assert(MT == 8 || MT == 16, "large-cell stream needs M = 8 or 16");
     constexpr int kCh = ring_chunk<MT>();
-    constexpr int kPer = kCh / NT;
+    constexpr int kPer = kCh / BT;
     constexpr int R = 32 / MT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    Smem &S = *reinterpret_cast<Smem *>(smem_raw);
-    float *tab = reinterpret_cast<float *>(smem_raw + sizeof(Smem));  // [K][M][R] replicated fold
+    ScanSmem<BT> &S = *reinterpret_cast<ScanSmem<BT> *>(smem_raw);
+    float *tab = reinterpret_cast<float *>(smem_raw + ((sizeof(ScanSmem<BT>) + 15) & ~(size_t)15));  // replicated fold
     unsigned long long *tk = reinterpret_cast<unsigned long long *>(smem_raw + A.tk_off);
     uint8_t *stc = smem_raw + A.tk_off + (size_t)A.tkcap * 8;      // [kRingS][kCh][MT] codes
     float *stp = reinterpret_cast<float *>(stc + (size_t)kRingS * kCh * MT);  // [kRingS][kCh] point terms
@@ -2325,7 +2360,7 @@ __global__ void __launch_bounds__(NT, 2) big_scan_kernel(Args<KT, OffT> A) {
         }
         // replicated fold table and the small cells' top-k
         const float *fq = A.fold + (size_t)qi * MT * K;
-        for (int x = threadIdx.x; x < MT * K; x += NT) {
+        for (int x = threadIdx.x; x < MT * K; x += BT) {
             const int p = x / K, c = x - p * K;
             const float v = __ldg(fq + x);
 #pragma unroll
@@ -2333,7 +2368,7 @@ __global__ void __launch_bounds__(NT, 2) big_scan_kernel(Args<KT, OffT> A) {
         }
         const uint32_t n0 = A.tk_n[qi];
         unsigned long long mx = 0;
-        for (uint32_t x = threadIdx.x; x < n0; x += NT) {
+        for (uint32_t x = threadIdx.x; x < n0; x += BT) {
             const unsigned long long key = A.tk_part[(size_t)qi * k + x];
             tk[x] = key;
             mx = key > mx ? key : mx;
@@ -2347,7 +2382,7 @@ __global__ void __launch_bounds__(NT, 2) big_scan_kernel(Args<KT, OffT> A) {
         __syncthreads();
         if (threadIdx.x == 0) {
             unsigned long long m = 0;
-            for (int w = 0; w < NW; w++) m = S.red[w] > m ? S.red[w] : m;
+            for (int w = 0; w < BT / 32; w++) m = S.red[w] > m ? S.red[w] : m;
             S.ntk = n0;
             // k keys held: the k-th smallest (their max) is the admission bound
             S.thr = n0 >= (uint32_t)k ? m : ~0ull;
@@ -2400,7 +2435,7 @@ __global__ void __launch_bounds__(NT, 2) big_scan_kernel(Args<KT, OffT> A) {
             float ptv[kPer], acc[kPer];
 #pragma unroll
             for (int u = 0; u < kPer; u++) {
-                const int j = u * NT + threadIdx.x;
+                const int j = u * BT + threadIdx.x;
                 if constexpr (MT == 16) {
                     const uint4 v = *reinterpret_cast<const uint4 *>(stc + ((size_t)slot * kCh + j) * MT);
                     w[u][0] = v.x; w[u][1] = v.y; w[u][2] = v.z; w[u][3] = v.w;
@@ -2413,7 +2448,7 @@ __global__ void __launch_bounds__(NT, 2) big_scan_kernel(Args<KT, OffT> A) {
             if (c_c + (uint32_t)kCh > b1 && end > b1) {
 #pragma unroll
                 for (int u = 0; u < kPer; u++) {
-                    const uint32_t e = c_c + u * NT + threadIdx.x;
+                    const uint32_t e = c_c + u * BT + threadIdx.x;
                     if (e >= b1 && e < end) {
                         load_code<MT>(A.codes + (size_t)e * MT, w[u], MT);
                         ptv[u] = __ldg(A.pterm + e);
@@ -2424,7 +2459,7 @@ __global__ void __launch_bounds__(NT, 2) big_scan_kernel(Args<KT, OffT> A) {
             for (int u = 0; u < kPer; u++) acc[u] = dist_pt_rep<MT>(tabb, offb, rot, cb, ptv[u], w[u]);
 #pragma unroll
             for (int u = 0; u < kPer; u++) {
-                const uint32_t e = c_c + u * NT + threadIdx.x;
+                const uint32_t e = c_c + u * BT + threadIdx.x;
                 const uint32_t db = canon_bits(acc[u]);
                 if (e >= lst && e < end && db <= thr_hi) {
                     const unsigned long long kk = ((unsigned long long)db << 32) | __ldg(A.ids + e);
@@ -2439,13 +2474,339 @@ __global__ void __launch_bounds__(NT, 2) big_scan_kernel(Args<KT, OffT> A) {
             __syncthreads();
             if (S.ntk > (uint32_t)(A.tkcap - kCh)) {
                 PROF(PH_BCOMPACT);
-                topk_compact(S, tk, k);
+                topk_compact<BT>(S, tk, k);
             }
         }
         PROF(PH_BFIN);
-        topk_compact(S, tk, k);
+        topk_compact<BT>(S, tk, k);
         const int64_t qo = A.q0 + qi;
-        write_topk(S, tk, k, A.ncand_q[qi], A.out_d + qo * k, A.out_ids + qo * k, A.out_count + qo);
+        write_topk<BT>(S, tk, k, A.ncand_q[qi], A.out_d + qo * k, A.out_ids + qo * k, A.out_count + qo);
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------------
+// Warp-independent large-cell stream (k <= kStreamMaxK).  Same ring and
+// lane mapping as big_scan_kernel, but no CTA barrier per chunk: each warp
+// scores its own 1/8 of every chunk and keeps its own top-k candidates in
+// a private shared-memory region (warp ballots append, a warp-level radix
+// select compacts), and the LAST warp to finish a chunk refills its stage
+// (an arrival counter per stage), so warps drift up to the ring depth apart
+// instead of waiting for the slowest at every chunk.  The tightest per-warp
+// k-th key is published (atomicMin) as a bound every warp admits against.
+// The warps' lists and the traversal kernel's list are merged once per
+// query by the CTA top-k.
+constexpr int kStreamMaxK = 256;
+constexpr int kCapW = 384;   // per-warp top-k region (keys)
+constexpr int kPlan = 512;   // cells whose chunk plan is staged at a time
+
+struct __align__(16) StreamSmem {
+    unsigned long long mbar[kRingS];
+    uint32_t done[kRingS];
+    uint32_t plan[kPlan + 1];  // chunk prefix over the batch's cells
+    unsigned long long gthr;   // admission bound: min over warps of their k-th key
+    uint32_t wcnt[NW];
+    uint32_t wscan[NW];
+    int64_t qidx;
+    // CTA top-k (topk_compact / write_topk)
+    uint32_t hist_c[256];
+    unsigned long long red[NW];
+    unsigned long long tor[NW];
+    unsigned long long thr;
+    uint32_t ntk;
+    int tsel_v;
+    uint32_t tcnt;
+    unsigned long long tsel_below;
+    unsigned long long tkey;
+    uint32_t nholes;
+    uint16_t holes[kMaxK];
+    int prof_ph;
+    long long prof_t;
+};
+
+// k-th smallest of a warp's n (> k) unique keys in tkw[0, n), n <= kCapW:
+// MSB-first bit construction with warp-wide counts, then the k survivors
+// are packed to tkw[0, k).  Returns the k-th key (the warp's admission bound).
+__device__ unsigned long long warp_topk(unsigned long long *tkw, uint32_t n, int k) {
+    constexpr int PER = kCapW / 32;
+    const int lane = threadIdx.x & 31;
+    unsigned long long key[PER];
+    unsigned long long ka = ~0ull, ko = 0ull;
+#pragma unroll
+    for (int i = 0; i < PER; i++) {
+        const uint32_t idx = lane + 32 * i;
+        key[i] = idx < n ? tkw[idx] : ~0ull;
+        if (idx < n) {
+            ka &= key[i];
+            ko |= key[i];
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        ka &= __shfl_xor_sync(0xffffffffu, ka, o);
+        ko |= __shfl_xor_sync(0xffffffffu, ko, o);
+    }
+    const int hb = 63 - __clzll((long long)(ka ^ ko));  // keys unique: ka != ko
+    unsigned long long v = hb >= 63 ? 0ull : (ka & ~((2ull << hb) - 1));
+    for (int b = hb; b >= 0; b--) {
+        const unsigned long long cand = v | ((1ull << b) - 1);
+        uint32_t c = 0;
+#pragma unroll
+        for (int i = 0; i < PER; i++) c += key[i] <= cand ? 1u : 0u;
+        c = __reduce_add_sync(0xffffffffu, c);
+        if (c < (uint32_t)k) v |= 1ull << b;
+    }
+    __syncwarp();
+    uint32_t pos = 0;
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int i = 0; i < PER; i++) {
+        const bool keep = key[i] <= v;
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (keep) tkw[pos + __popc(bal & lt)] = key[i];
+        pos += __popc(bal);
+    }
+    __syncwarp();
+    return v;
+}
+
+template <int MT, typename KT, typename OffT>
+__global__ void __launch_bounds__(NT, 2) big_stream_kernel(Args<KT, OffT> A) {
+    static_assert(MT == 8 || MT == 16, "large-cell stream needs M = 8 or 16");
+    constexpr int kCh = ring_chunk<MT>();
+    constexpr int kPerW = kCh / NW;  // entries per warp per chunk
+    constexpr int kPer = kPerW / 32;  // per lane
+    constexpr int R = 32 / MT;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    StreamSmem &S = *reinterpret_cast<StreamSmem *>(smem_raw);
+    float *tab = reinterpret_cast<float *>(smem_raw + ((sizeof(StreamSmem) + 15) & ~(size_t)15));
+    unsigned long long *tkall = reinterpret_cast<unsigned long long *>(smem_raw + A.tk_off);  // [NW][kCapW]
+    uint8_t *stc = reinterpret_cast<uint8_t *>(tkall + NW * kCapW);                       // [kRingS][kCh][MT]
+    float *stp = reinterpret_cast<float *>(stc + (size_t)kRingS * kCh * MT);               // [kRingS][kCh]
+    const int K = A.K, k = A.k;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const uint32_t nal = A.n_local & ~3u;
+    unsigned long long *tkw = tkall + warp * kCapW;
+    const char *tabb = reinterpret_cast<const char *>(tab);
+    int offb[MT];
+    int rot;
+    {
+        const LaneLut<MT> L(lane);
+        rot = L.rot;
+#pragma unroll
+        for (int i = 0; i < MT; i++) offb[i] = L.off[i] * 4;
+    }
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < kRingS; st++) {
+            mbar_init(&S.mbar[st], 1);
+            S.done[st] = 0;
+        }
+        mbar_fence_init();
+#ifdef BPQ_PHASE_PROF
+        S.prof_ph = PH_IDLE;
+        S.prof_t = clock64();
+#endif
+    }
+    uint32_t base = 0;  // chunks streamed so far by this CTA (stage = base % kRingS, parity = base / kRingS)
+    for (;;) {
+        PROF(PH_BPRO);
+        if (threadIdx.x == 0) {
+            const unsigned int c = atomicAdd(A.counter, 1u);
+            S.qidx = c < *A.bigq_count ? (int64_t)A.bigq_list[c] : (int64_t)-1;
+        }
+        __syncthreads();
+        const int64_t qi = S.qidx;
+        if (qi < 0) {
+            PROF(PH_IDLE);
+            return;
+        }
+        const float *fq = A.fold + (size_t)qi * MT * K;
+        for (int x = threadIdx.x; x < MT * K; x += NT) {
+            const int p = x / K, c = x - p * K;
+            const float v = __ldg(fq + x);
+#pragma unroll
+            for (int r = 0; r < R; r++) tab[fold_index<MT>(p, c, K) + r] = v;
+        }
+        // the traversal kernel's k-th key (if it holds k) bounds admission from the start
+        const uint32_t n0 = A.tk_n[qi];
+        unsigned long long mx = 0;
+        for (uint32_t x = threadIdx.x; x < n0; x += NT) {
+            const unsigned long long key = A.tk_part[(size_t)qi * k + x];
+            mx = key > mx ? key : mx;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long y = __shfl_xor_sync(0xffffffffu, mx, o);
+            mx = y > mx ? y : mx;
+        }
+        if (lane == 0) S.red[warp] = mx;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long m = 0;
+            for (int w = 0; w < NW; w++) m = S.red[w] > m ? S.red[w] : m;
+            S.gthr = n0 >= (uint32_t)k ? m : ~0ull;
+        }
+        __syncthreads();
+        uint32_t wcnt = 0;
+        unsigned long long wthr = ~0ull;
+        const int4 *cells = A.big_cells + (size_t)qi * A.big_cap;
+        const uint32_t nb = A.big_n[qi];
+        for (uint32_t xb = 0; xb < nb; xb += kPlan) {
+            const uint32_t nbb = min((uint32_t)kPlan, nb - xb);
+            // chunk plan: prefix of each cell's chunk count (chunks start at a 32-entry boundary)
+            {
+                constexpr int PT = (kPlan + NT - 1) / NT;
+                uint32_t cnt[PT], sum = 0;
+#pragma unroll
+                for (int i = 0; i < PT; i++) {
+                    const uint32_t x = threadIdx.x * PT + i;
+                    cnt[i] = 0;
+                    if (x < nbb) {
+                        const int4 cl = __ldg(&cells[xb + x]);
+                        const uint32_t c0 = (uint32_t)cl.x & ~31u, end = (uint32_t)cl.x + (uint32_t)cl.y;
+                        cnt[i] = (end - c0 + kCh - 1) / kCh;
+                    }
+                    sum += cnt[i];
+                }
+                uint32_t tot;
+                uint32_t ex = block_excl_scan(S, sum, &tot);
+#pragma unroll
+                for (int i = 0; i < PT; i++) {
+                    const uint32_t x = threadIdx.x * PT + i;
+                    if (x < nbb) S.plan[x] = ex;
+                    ex += cnt[i];
+                }
+                if (threadIdx.x == 0) S.plan[nbb] = tot;
+            }
+            __syncthreads();
+            const uint32_t C = S.plan[nbb];
+            // chunk c of the batch -> stage (base + c) % kRingS, by whichever thread issues it
+            auto issue = [&](uint32_t c) {
+                int lo = 0, hi = (int)nbb;  // largest x with plan[x] <= c
+                while (hi - lo > 1) {
+                    const int mid = (lo + hi) >> 1;
+                    if (S.plan[mid] <= c) lo = mid; else hi = mid;
+                }
+                const int4 cl = __ldg(&cells[xb + lo]);
+                const uint32_t end = (uint32_t)cl.x + (uint32_t)cl.y;
+                const uint32_t c0 = ((uint32_t)cl.x & ~31u) + (c - S.plan[lo]) * (uint32_t)kCh;
+                const uint32_t b1 = min(min(c0 + (uint32_t)kCh, (end + 3u) & ~3u), nal);
+                const uint32_t n = b1 > c0 ? b1 - c0 : 0u;
+                const int slot = (int)((base + c) % kRingS);
+                unsigned long long *bar = &S.mbar[slot];
+                fence_proxy_async();
+                mbar_arrive_tx(bar, n * (MT + 4));
+                if (n) {
+                    bulk_g2s(stc + (size_t)slot * kCh * MT, A.codes + (size_t)c0 * MT, n * MT, bar);
+                    bulk_g2s(stp + (size_t)slot * kCh, A.pterm + c0, n * 4, bar);
+                }
+            };
+            if (threadIdx.x == 0)
+                for (uint32_t c = 0; c < C && c < (uint32_t)kRingS; c++) issue(c);
+            uint32_t x = 0;  // this warp's cell cursor
+            for (uint32_t c = 0; c < C; c++) {
+                const uint32_t gc = base + c;
+                const int slot = (int)(gc % kRingS);
+                PROF(PH_BWAIT);
+                mbar_wait(&S.mbar[slot], (gc / kRingS) & 1u);
+                PROF(PH_BSCORE);
+                while (S.plan[x + 1] <= c) x++;
+                const int4 cl = __ldg(&cells[xb + x]);
+                const uint32_t lst = (uint32_t)cl.x, end = lst + (uint32_t)cl.y;
+                const float cb = __int_as_float(cl.z);
+                const uint32_t c0 = (lst & ~31u) + (c - S.plan[x]) * (uint32_t)kCh;
+                const uint32_t b1 = min(min(c0 + (uint32_t)kCh, (end + 3u) & ~3u), nal);
+                uint32_t w[kPer][4];
+                float ptv[kPer], acc[kPer];
+#pragma unroll
+                for (int u = 0; u < kPer; u++) {
+                    const int j = warp * kPerW + u * 32 + lane;
+                    if constexpr (MT == 16) {
+                        const uint4 v = *reinterpret_cast<const uint4 *>(stc + ((size_t)slot * kCh + j) * MT);
+                        w[u][0] = v.x; w[u][1] = v.y; w[u][2] = v.z; w[u][3] = v.w;
+                    } else {
+                        const uint2 v = *reinterpret_cast<const uint2 *>(stc + ((size_t)slot * kCh + j) * MT);
+                        w[u][0] = v.x; w[u][1] = v.y; w[u][2] = 0; w[u][3] = 0;
+                    }
+                    ptv[u] = stp[slot * kCh + j];
+                }
+                if (c0 + (uint32_t)kCh > b1 && end > b1) {
+#pragma unroll
+                    for (int u = 0; u < kPer; u++) {
+                        const uint32_t e = c0 + warp * kPerW + u * 32 + lane;
+                        if (e >= b1 && e < end) {
+                            load_code<MT>(A.codes + (size_t)e * MT, w[u], MT);
+                            ptv[u] = __ldg(A.pterm + e);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kPer; u++) acc[u] = dist_pt_rep<MT>(tabb, offb, rot, cb, ptv[u], w[u]);
+                // admission against min(own k-th key, published bound); ids only for candidates
+                const unsigned long long g = S.gthr;
+                const unsigned long long bound = wthr < g ? wthr : g;
+                const uint32_t bhi = (uint32_t)(bound >> 32);
+#pragma unroll
+                for (int u = 0; u < kPer; u++) {
+                    const uint32_t e = c0 + warp * kPerW + u * 32 + lane;
+                    const uint32_t db = canon_bits(acc[u]);
+                    bool pass = e >= lst && e < end && db <= bhi;
+                    unsigned long long kk = 0;
+                    if (pass) {
+                        kk = ((unsigned long long)db << 32) | __ldg(A.ids + e);
+                        pass = kk < bound;
+                    }
+                    const unsigned bal = __ballot_sync(0xffffffffu, pass);
+                    if (pass) tkw[wcnt + __popc(bal & lt)] = kk;
+                    wcnt += __popc(bal);
+                }
+                __syncwarp();
+                // release the stage; the last warp through refills it
+                if (lane == 0) {
+                    __threadfence_block();
+                    const uint32_t old = atomicAdd(&S.done[slot], 1u);
+                    if (old == NW - 1) {
+                        __threadfence_block();
+                        S.done[slot] = 0;
+                        if (c + kRingS < C) issue(c + kRingS);
+                    }
+                }
+                if (wcnt > (uint32_t)(kCapW - kPerW)) {
+                    PROF(PH_BCOMPACT);
+                    wthr = warp_topk(tkw, wcnt, k);
+                    wcnt = (uint32_t)k;
+                    if (lane == 0) atomicMin(&S.gthr, wthr);
+                }
+            }
+            base += C;
+            __syncthreads();  // batch done: every stage drained
+        }
+        // merge: each warp's list (<= k after a final select) and the traversal kernel's list
+        PROF(PH_BFIN);
+        if (wcnt > (uint32_t)k) {
+            warp_topk(tkw, wcnt, k);
+            wcnt = (uint32_t)k;
+        }
+        if (lane == 0) S.wcnt[warp] = wcnt;
+        __syncthreads();
+        unsigned long long *m = reinterpret_cast<unsigned long long *>(stc);  // the drained ring
+        uint32_t off = 0;
+        for (int w2 = 0; w2 < NW; w2++) {
+            const uint32_t cw = S.wcnt[w2];
+            for (uint32_t i = threadIdx.x; i < cw; i += NT) m[off + i] = tkall[w2 * kCapW + i];
+            off += cw;
+        }
+        for (uint32_t i = threadIdx.x; i < n0; i += NT) m[off + i] = A.tk_part[(size_t)qi * k + i];
+        off += n0;
+        if (threadIdx.x == 0) {
+            S.ntk = off;
+            S.thr = ~0ull;
+        }
+        __syncthreads();
+        topk_compact(S, m, k);
+        const int64_t qo = A.q0 + qi;
+        write_topk(S, m, k, A.ncand_q[qi], A.out_d + qo * k, A.out_ids + qo * k, A.out_count + qo);
         __syncthreads();
     }
 }
@@ -2626,23 +2987,38 @@ int launch_big_one(const Index &ix, const float *queries, int64_t q0, int64_t nq
         fill_args<BPQ_ENGINE_FBPQ, MT>(A, ix, queries, q0, nq, budget, k, ws, out_dist, out_ids, out_count,
                                        nullptr, nullptr);
         if (A.big_cells == nullptr) return BPQ_OK;
-        A.tkcap = ((k + 255) & ~255) + 2 * ring_chunk<MT>();  // compaction once per >= one chunk of offers
-        A.tk_off = (int)((sizeof(Smem) + (size_t)32 * ix.K * 4 + 15) & ~(size_t)15);
-        const size_t smem = (size_t)A.tk_off + (size_t)A.tkcap * 8 + ring_bytes<MT>();
-        auto kfn = big_scan_kernel<MT, float, uint32_t>;
+        // the warp-independent variant measured slower (per-warp compactions, looser
+        // admission); it stays available for A/B runs
+        constexpr int BT = 512;
+        const bool warp_mode = k <= kStreamMaxK && getenv("BPQ_STREAM_WARP") != nullptr;
+        size_t smem;
+        if (warp_mode) {
+            A.tkcap = kCapW;
+            A.tk_off = (int)((((sizeof(StreamSmem) + 15) & ~(size_t)15) + (size_t)32 * ix.K * 4 + 15) & ~(size_t)15);
+            smem = (size_t)A.tk_off + (size_t)NW * kCapW * 8 + ring_bytes<MT>();
+        } else {
+            A.tkcap = ((k + 255) & ~255) + 2 * ring_chunk<MT>();  // compaction once per >= one chunk of offers
+            A.tk_off = (int)((((sizeof(ScanSmem<BT>) + 15) & ~(size_t)15) + (size_t)32 * ix.K * 4 + 15) & ~(size_t)15);
+            smem = (size_t)A.tk_off + (size_t)A.tkcap * 8 + ring_bytes<MT>();
+        }
+        auto kfn = warp_mode ? big_stream_kernel<MT, float, uint32_t> : big_scan_kernel<MT, BT, float, uint32_t>;
+        const int threads = warp_mode ? NT : BT;
         static bool attr = false;
         if (!attr) {
             int dev = 0, optin = 0;
             BPQ_CUDA_TRY(cudaGetDevice(&dev));
             BPQ_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-            BPQ_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+            BPQ_CUDA_TRY(cudaFuncSetAttribute(big_stream_kernel<MT, float, uint32_t>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+            BPQ_CUDA_TRY(cudaFuncSetAttribute(big_scan_kernel<MT, BT, float, uint32_t>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
             attr = true;
         }
         int occ = 0;
-        BPQ_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, NT, smem));
+        BPQ_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, threads, smem));
         if (occ < 1) return fail(BPQ_ERR_UNSUPPORTED, "large-cell stream shared memory does not fit on an SM");
         BPQ_CUDA_TRY(cudaMemsetAsync(ws.counter, 0, sizeof(unsigned int), stream));
-        kfn<<<occ * num_sms(), NT, smem, stream>>>(A);
+        kfn<<<occ * num_sms(), threads, smem, stream>>>(A);
         BPQ_CUDA_TRY(cudaGetLastError());
         return BPQ_OK;
     }

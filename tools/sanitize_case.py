@@ -1,7 +1,9 @@
 """Small end-to-end workload for compute-sanitizer (racecheck / memcheck /
-synccheck): config-0 FBPQ + Multi-D-ADC searches (dense traversal), and a
-sparse T=1500 index that exercises the partial sort, the in-kernel prefix
-extension, the retry pass and the top-k compaction."""
+synccheck): config-0 FBPQ + Multi-D-ADC searches (tensor-core first layer,
+dense traversal), a sparse T=1500 index that exercises the partial sort, the
+in-kernel prefix extension, the retry pass and the top-k compaction, a
+large-cell M=8 index through the TMA stream kernels (warp-mode k=100 and
+CTA-mode k=300, unaligned array end), and a tie plateau (plateau windows)."""
 import sys
 from pathlib import Path
 
@@ -32,5 +34,27 @@ sp = DeviceIndex(c1=c1, c2=c2, offsets=off, ids=ids, codes=codes, books=books)
 qs = (cent[rng.integers(0, 300, 6)] + rng.normal(size=(6, dim))).astype(np.float32)
 for L in (100, 5000, n):
     sp.search(qs, L, 50, "fbpq").numpy()
+# large cells, M = 8: the TMA stream (warp mode for k <= 256, CTA mode above)
+t, dim, m, kk, n = 10, 32, 8, 32, 20_003
+base = rng.normal(size=(n, dim)).astype(np.float32)
+c1 = base[rng.choice(n, t, replace=False), : dim // 2].copy()
+c2 = base[rng.choice(n, t, replace=False), dim // 2 :].copy()
+books = (0.3 * rng.normal(size=(m, kk, dim // m))).astype(np.float32)
+off, ids, codes = orc.build_index(base, c1, c2, books)
+lc = DeviceIndex(c1=c1, c2=c2, offsets=off, ids=ids, codes=codes, books=books)
+ql = rng.normal(size=(6, dim)).astype(np.float32)
+for L, k in ((2000, 100), (n, 300)):
+    lc.search(ql, L, k, "fbpq").numpy()
+# tie plateau: 192 codewords per half at +-10 e_u, query at the origin (every key equal, 36,864 cells)
+dh, t = 96, 192
+cb = np.zeros((t, dh), np.float32)
+for i in range(t):
+    cb[i, i // 2] = 10.0 if i % 2 == 0 else -10.0
+ii, jj = np.meshgrid(np.arange(t), np.arange(t), indexing="ij")
+base = np.concatenate([cb[ii.ravel()], cb[jj.ravel()]], 1) + rng.normal(scale=0.01, size=(t * t, 2 * dh)).astype(np.float32)
+books = (0.01 * rng.normal(size=(8, 16, 2 * dh // 8))).astype(np.float32)
+off, ids, codes = orc.build_index(base.astype(np.float32), cb, cb, books)
+pl = DeviceIndex(c1=cb, c2=cb, offsets=off, ids=ids, codes=codes, books=books, exact=True)
+pl.search(np.zeros((2, 2 * dh), np.float32), 5000, 20, "fbpq").numpy()
 torch.cuda.synchronize()
 print("sanitize case done")
