@@ -232,6 +232,41 @@ def build_ref_books_workload(cfg, device, rank, t0):
     return dix, q, host
 
 
+def build_sharded_ref_workload(cfg, device, rank, world):
+    """c1/c2 sharded by point id: rank r encodes rows [r N / W, (r+1) N / W) of
+    the same blocked base stream with the reference-trained codebooks (ids
+    offset by the range start); the global per-cell counts come from one NCCL
+    all-reduce.  Queries are the same 10k on every rank."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1404_1831_b200 import DeviceIndex, datagen, encode
+
+    bk = np.load(ROOT / "tests" / "golden" / "c1_books.npz")
+    c1, c2, books = bk["c1"], bk["c2"], bk["books"]
+    cent = datagen.mixture_centres(cfg["ncomp"], cfg["dim"])
+    lo, hi = cfg["n"] * rank // world, cfg["n"] * (rank + 1) // world
+    blocks = []
+    for b in range(lo // datagen.BLOCK, (hi - 1) // datagen.BLOCK + 1):
+        b0 = b * datagen.BLOCK
+        rows = min(cfg["n"], b0 + datagen.BLOCK) - b0
+        x = datagen.clipped_mixture_block(b, cfg["dim"], cfg["ncomp"], datagen.SEED_BASE, cent, rows)
+        blocks.append(x[max(lo - b0, 0): min(hi - b0, rows)])
+    base = torch.from_numpy(np.concatenate(blocks)).to(device)
+    local = encode.build_index(base, c1, c2, books, id_offset=lo, device=device)
+    del base
+    cnt = (local.offsets[1:].long() & 0xFFFFFFFF) - (local.offsets[:-1].long() & 0xFFFFFFFF)
+    dist.all_reduce(cnt)
+    goff = torch.zeros(cnt.numel() + 1, dtype=torch.int64, device=device)
+    torch.cumsum(cnt, 0, out=goff[1:])
+    dix = DeviceIndex(c1=c1, c2=c2, offsets=local.offsets, ids=local.ids, codes=local.codes, books=books,
+                      tables=(local.cn1, local.cn2, local.fine_norms, local.cross1, local.cross2),
+                      global_offsets=goff.to(torch.int32), num_entries_global=int(goff[-1].item()), device=device)
+    del local
+    qh = datagen.clipped_mixture_block(0, cfg["dim"], cfg["ncomp"], datagen.SEED_QUERIES, cent, cfg["nq"])
+    return dix, torch.from_numpy(qh).to(device)
+
+
 def build_sharded_workload(cfg, device, rank, world):
     """rank r holds the points with ids in [r N / W, (r+1) N / W)
     (its own multi-index, built with id_offset) plus the GLOBAL per-cell
@@ -423,7 +458,8 @@ def _config_block(cfg, n, dim, t, m, kk, nq, args, world):
     engine, L, k = cfg["engine"], cfg["L"], cfg["topk"]
     workload = f"{cfg['name']}: {engine} N={n:,} D={dim} T={t} M={m}x{kk} nq={nq} L={L} k={k}"
     return {"workload": workload, "engine": engine, "N": n, "D": dim, "T": t, "M": m, "nq": nq, "L": L, "k": k,
-            "parallelism": (f"shard{world}" if args.shard else f"replicas{args.gpus}" if world > 1 else "single"),
+            "parallelism": ((f"shard{world}" + ("" if args.no_split else "+query-split")) if args.shard
+                            else f"replicas{args.gpus}" if world > 1 else "single"),
             "l2": "flushed between timed steps (256 MiB write)"}
 
 
@@ -444,7 +480,13 @@ def main():
     ap.add_argument("--exact", action="store_true", help="FBPQ/Multi-D-ADC/HBPQ in the reference's exact "
                     "operation order (no point term, no per-cell residual tables)")
     ap.add_argument("--shard", action="store_true",
-                    help="shard the database by point id across the ranks (global budget, NCCL all-gather merge)")
+                    help="shard the database by point id across the ranks (global budget, NCCL all-gather merge); "
+                         "the default when launched with more than one rank")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: every rank searches its own batch over a full copy instead (weak scaling)")
+    ap.add_argument("--no-split", action="store_true",
+                    help="sharded: replicate the first layer and traversal on every rank instead of splitting the "
+                         "queries across ranks for them")
     ap.add_argument("--phase-profile", action="store_true",
                     help="print per-phase cycle shares of the fused kernel (needs BPQ_LIB=...libbpq_b200_prof.so)")
     args = ap.parse_args()
@@ -453,6 +495,8 @@ def main():
     RECALL_Q = args.recall_queries
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world > 1 and not args.replicas:
+        args.shard = True  # north_star's scaling path: the database sharded by point id
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     cfg = _config(args)
     if args.exact:
@@ -486,9 +530,12 @@ def main():
     if args.shard:
         from paper_1404_1831_b200 import sharded
 
-        dix, q = build_sharded_workload(cfg, device, rank, world)
+        dix, q = (build_sharded_ref_workload if cfg.get("ref_books") else build_sharded_workload)(cfg, device, rank,
+                                                                                                   world)
         host = None
-        searcher = sharded.ShardedSearcher(dix, force_collective=True)
+        split = (not args.no_split and engine == "fbpq" and dix.m in (8, 16) and not dix.fbpq_exact)
+        searcher = (sharded.SplitSearcher(dix, force_collective=True) if split
+                    else sharded.ShardedSearcher(dix, force_collective=True))
     else:
         dix, q, host = build_workload(cfg, device, rank)
     nq = q.shape[0]

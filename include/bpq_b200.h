@@ -229,6 +229,28 @@ int bpq_merge_topk(const float *dists, const uint32_t *ids, const int32_t *count
                    int64_t nq, int32_t k, float *out_dist, uint32_t *out_ids,
                    int32_t *out_count, void *stream);
 
+/* Query-split sharding (the traversal divided across ranks).
+ * Rank r traverses only its query slice against the global cell counts and
+ * records every visited non-empty cell instead of scanning it:
+ * bpq_search_split_traverse writes visits [nq][cap] as int4
+ * (oi * T + oj, global count, cell_base f32 bits, 0) in visit order and
+ * visit_count [nq] (0xFFFFFFFF: the query failed); cap >=
+ * bpq_split_visit_cap(index, budget).  After the ranks all-gather the
+ * packed lists (visit_start [nq + 1] over all queries, rank order), each rank
+ * streams its local entries of every query's cells with
+ * bpq_search_split_scan (point-term FBPQ, M = 8 / 16), giving per-rank
+ * [nq, k] lists for the usual merge.  Workspace: bpq_search_workspace_size
+ * for the traversal, bpq_split_scan_workspace_size for the scan. */
+int64_t bpq_split_visit_cap(const bpq_index *index, int64_t budget);
+int bpq_search_split_traverse(const bpq_index *index, const float *queries, int64_t nq, int64_t budget,
+                              uint32_t *visit_count, void *visits, int64_t cap, int64_t *out_ncand,
+                              void *workspace, size_t workspace_bytes, void *stream);
+size_t bpq_split_scan_workspace_size(const bpq_index *index, int64_t nq, int64_t total_visits);
+int bpq_search_split_scan(const bpq_index *index, const float *queries, int64_t nq, int32_t k,
+                          const void *visits, const uint32_t *visit_start, int64_t total_visits,
+                          float *out_dist, uint32_t *out_ids, int32_t *out_count, void *workspace,
+                          size_t workspace_bytes, void *stream);
+
 /* The same merge over the packed buffer of one all-gather: shard s occupies
  * words [s * W, (s + 1) * W), W = 2 * nq * k + nq, laid out as dists f32
  * [nq, k] | ids u32 [nq, k] | counts i32 [nq]. */

@@ -87,6 +87,10 @@ SIGNATURES = {
     "bpq_coarse_dots": (ctypes.c_int, [P, P, I64, P, P, P]),
     "bpq_merge_topk": (ctypes.c_int, [P, P, P, I32, I64, I32, P, P, P, P]),
     "bpq_merge_topk_packed": (ctypes.c_int, [P, I32, I64, I32, P, P, P, P]),
+    "bpq_split_visit_cap": (I64, [P, I64]),
+    "bpq_search_split_traverse": (ctypes.c_int, [P, P, I64, I64, P, P, I64, P, P, SZ, P]),
+    "bpq_split_scan_workspace_size": (SZ, [P, I64, I64]),
+    "bpq_search_split_scan": (ctypes.c_int, [P, P, I64, I32, P, P, I64, P, P, P, P, SZ, P]),
 }
 
 _lib = None

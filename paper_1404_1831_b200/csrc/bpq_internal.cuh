@@ -51,6 +51,7 @@ struct Index {
     const float *books, *fine_norms, *cross1, *cross2, *bank1, *bank2;
     const float *rot, *rot1, *rot2;  // optional rotations (see bpq_index_desc)
     const float *pterm;  // FBPQ per-entry cross term [N] (null: exact reference-order scan)
+    const uint8_t *codes_rot;  // point-term FBPQ, M = 8 / 16: entry e's code bytes rotated by e % M
     // bf16 limb images of the coarse books for the tensor-core first layer (tc_dots.cu; null: FFMA)
     const uint8_t *cimg1, *cimg2;
     bool exact;          // bpq_index_desc.fbpq_exact: reference operation order, all engines
@@ -64,6 +65,7 @@ struct Index {
 // ---- launchers implemented in the .cu files --------------------------------
 int launch_point_term(const uint32_t *offsets, int32_t t, int32_t m, int32_t k, const uint8_t *codes,
                       const float *cross1, const float *cross2, float *pt, cudaStream_t s);
+int launch_rotate_codes(const uint8_t *codes, int64_t n, int32_t m, uint8_t *out, cudaStream_t s);
 int launch_coarse_dots(const float *queries, int64_t nq, int32_t D, const float *c1,
                        const float *c2, int32_t T, float *dots1, float *dots2,
                        cudaStream_t stream);
@@ -100,6 +102,10 @@ struct SearchWorkspace {
     unsigned long long *tk_part;   // [chunk][k]
     unsigned long long *ncand_q;   // [chunk]
     unsigned int *bigq_list, *bigq_count;
+    const uint32_t *big_start;     // split scan: packed per-query cell ranges [nq + 1] (else null)
+    int4 *record;                  // record mode (query-split traversal): [nq][record_cap] visited cells
+    uint32_t *record_n;
+    int record_cap;
     char *cta_scratch;
     size_t cta_stride;
     int n_cta;
@@ -109,6 +115,9 @@ size_t search_cta_scratch_bytes(int32_t T, int32_t D);
 int launch_rotate(const float *x, int64_t n, int32_t d, const float *R, float *out, cudaStream_t stream);
 int search_grid_ctas(int engine, int M);
 int effective_lut_min();
+int launch_visits_to_cells(const int4 *visits, const uint32_t *visit_start, int64_t nq, const uint32_t *loff,
+                           int4 *cells, uint32_t *cell_n, unsigned long long *ncand, uint32_t *tk_n,
+                           unsigned int *qlist, unsigned int *qcount, cudaStream_t s);
 int launch_big_scan(const Index &ix, int engine, const float *queries, int64_t q0, int64_t nq, int64_t budget,
                     int32_t k, const SearchWorkspace &ws, float *out_dist, uint32_t *out_ids, int32_t *out_count,
                     cudaStream_t stream);

@@ -32,7 +32,9 @@ struct SearchLayout {
 // large cells (>= lut_min entries) a query can visit: all but the cutoff cell lie inside the budget
 int64_t big_cells_cap(const Index &ix, int64_t budget) {
     // the stream kernel moves codes by TMA bulk copies: 16-byte aligned code array
-    if (!(ix.pterm != nullptr && (ix.M == 8 || ix.M == 16)) || (reinterpret_cast<uintptr_t>(ix.codes) & 15)) return 0;
+    if (!(ix.pterm != nullptr && ix.codes_rot != nullptr && (ix.M == 8 || ix.M == 16)) ||
+        (reinterpret_cast<uintptr_t>(ix.codes_rot) & 15))
+        return 0;
     return budget / std::max(effective_lut_min(), 1) + 2;
 }
 
@@ -242,6 +244,7 @@ extern "C" int bpq_index_create(const bpq_index_desc *d, int copy_from_host, bpq
         }
     }
     ix.pterm = nullptr;
+    ix.codes_rot = nullptr;
     ix.exact = d->fbpq_exact != 0;
     if (ix.cross1 && ix.cross2 && ix.codes && N > 0 && !d->fbpq_exact) {
         float *pt = nullptr;
@@ -265,6 +268,25 @@ extern "C" int bpq_index_create(const bpq_index_desc *d, int copy_from_host, bpq
             return fail(BPQ_ERR_CUDA, msg);
         }
         ix.pterm = pt;
+        if (ix.M == 8 || ix.M == 16) {
+            // the point-term scans read the codes pre-rotated (cells.cu rotate_codes_kernel)
+            void *cr = nullptr;
+            if (cudaMalloc(&cr, std::max<size_t>(N * M, 16)) != cudaSuccess) {
+                cudaGetLastError();
+                bpq_index_destroy(h);
+                return fail(BPQ_ERR_CUDA, "cannot allocate the rotated code array");
+            }
+            ix.owned.push_back(cr);
+            int rc = launch_rotate_codes(ix.codes, N, ix.M, static_cast<uint8_t *>(cr), 0);
+            if (rc == BPQ_OK && cudaDeviceSynchronize() != cudaSuccess)
+                rc = fail(BPQ_ERR_CUDA, cudaGetErrorString(cudaGetLastError()));
+            if (rc) {
+                std::string msg = g_last_error;
+                bpq_index_destroy(h);
+                return fail(BPQ_ERR_CUDA, msg);
+            }
+            ix.codes_rot = static_cast<uint8_t *>(cr);
+        }
     }
     *out = h;
     return BPQ_OK;
@@ -297,11 +319,13 @@ extern "C" int bpq_search(const bpq_index *index, int engine, const float *queri
                          out_ncand, nullptr, nullptr, workspace, workspace_bytes, stream);
 }
 
-extern "C" int bpq_search_ex(const bpq_index *index, int engine, const float *queries, int64_t nq,
-                             int64_t budget, int32_t k, float *out_dist, uint32_t *out_ids,
-                             int32_t *out_count, int64_t *out_ncand, int64_t *out_popped,
-                             void *const *stage_events, void *workspace, size_t workspace_bytes,
-                             void *stream) {
+namespace {
+// The batched search; with rec != nullptr (query-split traversal) every visited non-empty cell is
+// recorded into rec [nq][rec_cap] (counts rec_n) instead of scanned, and no top-k is produced.
+int search_impl(const bpq_index *index, int engine, const float *queries, int64_t nq, int64_t budget, int32_t k,
+                float *out_dist, uint32_t *out_ids, int32_t *out_count, int64_t *out_ncand, int64_t *out_popped,
+                void *const *stage_events, void *workspace, size_t workspace_bytes, void *stream, int4 *rec,
+                uint32_t *rec_n, int64_t rec_cap) {
     BPQ_CHECK(index != nullptr, BPQ_ERR_INVALID, "null index");
     const Index &ix = index->ix;
     // traverse() rejects budget < 1 (multi_index.py:308-309); search_* reject r < 1
@@ -351,7 +375,11 @@ extern "C" int bpq_search_ex(const bpq_index *index, int engine, const float *qu
     ws.counter = reinterpret_cast<unsigned int *>(w + L.counter);
     ws.big_cells = nullptr;
     ws.big_cap = 0;
-    if (L.big_cap) {
+    ws.big_start = nullptr;
+    ws.record = nullptr;
+    ws.record_n = nullptr;
+    ws.record_cap = 0;
+    if (L.big_cap && rec == nullptr) {
         ws.big_cells = reinterpret_cast<int4 *>(w + L.big);
         ws.big_cap = (int)L.big_cap;
         ws.big_n = reinterpret_cast<uint32_t *>(w + L.big_n);
@@ -369,6 +397,11 @@ extern "C" int bpq_search_ex(const bpq_index *index, int engine, const float *qu
     if (ev) BPQ_CUDA_TRY(cudaEventRecord((cudaEvent_t)stage_events[0], s));
     for (int64_t q0 = 0; q0 < nq; q0 += L.chunk) {
         int64_t n = std::min<int64_t>(L.chunk, nq - q0);
+        if (rec != nullptr) {
+            ws.record = rec + q0 * rec_cap;
+            ws.record_n = rec_n + q0;
+            ws.record_cap = (int)rec_cap;
+        }
         const float *qc = queries + q0 * ix.D;
         if (ix.rot) {  // queries into the index's rotated space (CoarsePair.rotate_in)
             int rr = launch_rotate(qc, n, ix.D, ix.rot, ws.qrot, s);
@@ -427,6 +460,99 @@ extern "C" int bpq_search_ex(const bpq_index *index, int engine, const float *qu
         if (ev) BPQ_CUDA_TRY(cudaEventRecord((cudaEvent_t)stage_events[4], s));
     }
     return BPQ_OK;
+}
+}  // namespace
+
+extern "C" int bpq_search_ex(const bpq_index *index, int engine, const float *queries, int64_t nq,
+                             int64_t budget, int32_t k, float *out_dist, uint32_t *out_ids,
+                             int32_t *out_count, int64_t *out_ncand, int64_t *out_popped,
+                             void *const *stage_events, void *workspace, size_t workspace_bytes,
+                             void *stream) {
+    return search_impl(index, engine, queries, nq, budget, k, out_dist, out_ids, out_count, out_ncand, out_popped,
+                       stage_events, workspace, workspace_bytes, stream, nullptr, nullptr, 0);
+}
+
+extern "C" int64_t bpq_split_visit_cap(const bpq_index *index, int64_t budget) {
+    if (!index || budget < 1) return 0;
+    const Index &ix = index->ix;
+    // every visited non-empty cell but the cutoff one lies inside the budget (>= 1 entry each)
+    int64_t cap = budget;
+    if (ix.populated > 0) cap = std::min<int64_t>(cap, ix.populated);
+    cap = std::min<int64_t>(cap, (int64_t)ix.T * ix.T);
+    return std::max<int64_t>(cap, 1);
+}
+
+extern "C" int bpq_search_split_traverse(const bpq_index *index, const float *queries, int64_t nq, int64_t budget,
+                                         uint32_t *visit_count, void *visits, int64_t cap, int64_t *out_ncand,
+                                         void *workspace, size_t workspace_bytes, void *stream) {
+    BPQ_CHECK(index != nullptr && visits != nullptr && visit_count != nullptr, BPQ_ERR_INVALID, "null argument");
+    BPQ_CHECK(cap >= bpq_split_visit_cap(index, budget), BPQ_ERR_INVALID, "visit capacity below bpq_split_visit_cap");
+    // k only sizes buffers that record mode does not use
+    return search_impl(index, BPQ_ENGINE_FBPQ, queries, nq, budget, 1, nullptr, nullptr, nullptr, out_ncand, nullptr,
+                       nullptr, workspace, workspace_bytes, stream, static_cast<int4 *>(visits), visit_count, cap);
+}
+
+extern "C" size_t bpq_split_scan_workspace_size(const bpq_index *index, int64_t nq, int64_t total_visits) {
+    if (!index || nq < 0 || total_visits < 0) return 0;
+    const Index &ix = index->ix;
+    size_t o = 0;
+    o += al((size_t)std::max<int64_t>(nq, 1) * ix.M * ix.K * 4);       // fold
+    o += al((size_t)std::max<int64_t>(total_visits, 1) * 16);          // local cells
+    o += 3 * al((size_t)std::max<int64_t>(nq, 1) * 4);                 // cell_n, tk_n, qlist
+    o += al((size_t)std::max<int64_t>(nq, 1) * 8);                     // ncand
+    o += al(8);                                                         // qcount, counter
+    o += ix.rot ? al((size_t)std::max<int64_t>(nq, 1) * ix.D * 4) : 0;  // rotated queries
+    return o;
+}
+
+extern "C" int bpq_search_split_scan(const bpq_index *index, const float *queries, int64_t nq, int32_t k,
+                                     const void *visits, const uint32_t *visit_start, int64_t total_visits,
+                                     float *out_dist, uint32_t *out_ids, int32_t *out_count, void *workspace,
+                                     size_t workspace_bytes, void *stream) {
+    BPQ_CHECK(index != nullptr, BPQ_ERR_INVALID, "null index");
+    const Index &ix = index->ix;
+    BPQ_CHECK(k >= 1 && k <= kMaxK, BPQ_ERR_INVALID, "k must be in [1, 1024]");
+    BPQ_CHECK(ix.pterm != nullptr && ix.codes_rot != nullptr && (ix.M == 8 || ix.M == 16), BPQ_ERR_UNSUPPORTED,
+              "the split scan streams point-term FBPQ cells (M = 8 or 16, fbpq_exact = 0)");
+    BPQ_CHECK(workspace_bytes >= bpq_split_scan_workspace_size(index, nq, total_visits), BPQ_ERR_WORKSPACE,
+              "split-scan workspace too small (see bpq_split_scan_workspace_size)");
+    if (nq == 0) return BPQ_OK;
+    char *w = static_cast<char *>(workspace);
+    size_t o = 0;
+    float *fold = reinterpret_cast<float *>(w + o); o += al((size_t)nq * ix.M * ix.K * 4);
+    int4 *cells = reinterpret_cast<int4 *>(w + o); o += al((size_t)std::max<int64_t>(total_visits, 1) * 16);
+    uint32_t *cell_n = reinterpret_cast<uint32_t *>(w + o); o += al((size_t)nq * 4);
+    uint32_t *tk_n = reinterpret_cast<uint32_t *>(w + o); o += al((size_t)nq * 4);
+    unsigned int *qlist = reinterpret_cast<unsigned int *>(w + o); o += al((size_t)nq * 4);
+    unsigned long long *ncand = reinterpret_cast<unsigned long long *>(w + o); o += al((size_t)nq * 8);
+    unsigned int *qcount = reinterpret_cast<unsigned int *>(w + o);
+    unsigned int *counter = qcount + 1; o += al(8);
+    cudaStream_t s = (cudaStream_t)stream;
+    const float *qc = queries;
+    if (ix.rot) {
+        float *qr = reinterpret_cast<float *>(w + o);
+        int rr = launch_rotate(queries, nq, ix.D, ix.rot, qr, s);
+        if (rr) return rr;
+        qc = qr;
+    }
+    int rc = launch_fold(qc, nq, ix.D, ix.M, ix.K, ix.books, ix.fine_norms, fold, s);
+    if (rc) return rc;
+    rc = launch_visits_to_cells(static_cast<const int4 *>(visits), visit_start, nq, ix.loff, cells, cell_n, ncand,
+                                tk_n, qlist, qcount, s);
+    if (rc) return rc;
+    SearchWorkspace ws{};
+    ws.fold = fold;
+    ws.big_cells = cells;
+    ws.big_start = visit_start;
+    ws.big_cap = 0;
+    ws.big_n = cell_n;
+    ws.tk_n = tk_n;
+    ws.tk_part = nullptr;
+    ws.ncand_q = ncand;
+    ws.bigq_list = qlist;
+    ws.bigq_count = qcount;
+    ws.counter = counter;
+    return launch_big_scan(ix, BPQ_ENGINE_FBPQ, qc, 0, nq, 1, k, ws, out_dist, out_ids, out_count, s);
 }
 
 extern "C" int bpq_coarse_dots(const bpq_index *index, const float *queries, int64_t nq, float *dots1, float *dots2,

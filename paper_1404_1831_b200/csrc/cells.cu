@@ -125,6 +125,82 @@ extern "C" int bpq_build_cell_lists(const uint32_t *offsets, int32_t t, uint32_t
 }
 
 namespace bpq {
+// codes_rot[e] = entry e's M code bytes rotated by e % M: byte i holds part
+// (e % M + i) % M (the order the point-term scans read them in, search_impl.cuh
+// LaneLut), so the scans skip the per-entry byte rotation
+__global__ void rotate_codes_kernel(const uint8_t *__restrict__ codes, int64_t n, int m, uint8_t *__restrict__ out) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n) return;
+    const int x = (int)(e % m);
+    const uint8_t *src = codes + e * m;
+    uint8_t *dst = out + e * m;
+    for (int i = 0; i < m; i++) dst[i] = src[(x + i) % m];
+}
+
+int launch_rotate_codes(const uint8_t *codes, int64_t n, int32_t m, uint8_t *out, cudaStream_t s) {
+    if (n <= 0) return BPQ_OK;
+    rotate_codes_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(codes, n, m, out);
+    BPQ_CUDA_TRY(cudaGetLastError());
+    return BPQ_OK;
+}
+
+// Query-split sharding: the visited cells of every query (all ranks'
+// traversals, packed by query) -> this shard's non-empty local cells
+// (start, count, cell_base) at the same packed positions, per-query counts
+// and local candidate counts, and the query list of the stream kernel.
+// One warp per query.
+__global__ void visits_to_cells_kernel(const int4 *__restrict__ visits, const uint32_t *__restrict__ vstart,
+                                       int64_t nq, const uint32_t *__restrict__ loff, int4 *__restrict__ cells,
+                                       uint32_t *__restrict__ cell_n, unsigned long long *__restrict__ ncand,
+                                       uint32_t *__restrict__ tk_n, unsigned int *__restrict__ qlist,
+                                       unsigned int *__restrict__ qcount) {
+    const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (q >= nq) return;
+    const uint32_t s = vstart[q], e = vstart[q + 1];
+    uint32_t n = 0;
+    unsigned long long cand = 0;
+    for (uint32_t i0 = s; i0 < e; i0 += 32) {
+        const uint32_t i = i0 + lane;
+        bool ok = false;
+        uint32_t l0 = 0, l1 = 0;
+        int4 v = make_int4(0, 0, 0, 0);
+        if (i < e) {
+            v = visits[i];
+            const uint32_t lin = (uint32_t)v.x;
+            l0 = __ldg(loff + lin);
+            l1 = __ldg(loff + lin + 1);
+            ok = l1 > l0;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, ok);
+        if (ok) {
+            cells[s + n + __popc(bal & ((1u << lane) - 1u))] = make_int4((int)l0, (int)(l1 - l0), v.z, 0);
+            cand += l1 - l0;
+        }
+        n += __popc(bal);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cand += __shfl_xor_sync(0xffffffffu, cand, o);
+    if (lane == 0) {
+        cell_n[q] = n;
+        ncand[q] = cand;
+        tk_n[q] = 0;
+        qlist[q] = (unsigned int)q;
+        if (q == 0) *qcount = (unsigned int)nq;
+    }
+}
+
+int launch_visits_to_cells(const int4 *visits, const uint32_t *visit_start, int64_t nq, const uint32_t *loff,
+                           int4 *cells, uint32_t *cell_n, unsigned long long *ncand, uint32_t *tk_n,
+                           unsigned int *qlist, unsigned int *qcount, cudaStream_t st) {
+    if (nq <= 0) return BPQ_OK;
+    const int64_t threads = nq * 32;
+    visits_to_cells_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(visits, visit_start, nq, loff, cells,
+                                                                             cell_n, ncand, tk_n, qlist, qcount);
+    BPQ_CUDA_TRY(cudaGetLastError());
+    return BPQ_OK;
+}
+
 int launch_point_term(const uint32_t *offsets, int32_t t, int32_t m, int32_t k, const uint8_t *codes,
                       const float *cross1, const float *cross2, float *pt, cudaStream_t s) {
     const size_t smem = (size_t)(m / 2) * k * sizeof(float);

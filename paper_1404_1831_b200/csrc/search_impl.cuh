@@ -208,6 +208,7 @@ struct Args {
     const uint8_t *codes;
     const float *books, *fine_norms, *cross1, *cross2, *bank1, *bank2;
     const float *pterm;        // FBPQ per-entry point term (null: exact reference order)
+    const uint8_t *codes_rot;  // codes with entry e's bytes rotated by e % M (point-term FBPQ, M = 8 / 16)
     // deferred large cells (point-term FBPQ, M = 8 / 16): the traversal kernel
     // records them here and big_scan_kernel streams them (null: scan in place)
     int4 *big_cells;           // [nq][big_cap] (start, count, cell_base bits, 0)
@@ -217,6 +218,12 @@ struct Args {
     uint32_t *tk_n;            // [nq]
     unsigned long long *ncand_q;  // [nq] candidate count (small + large cells)
     unsigned int *bigq_list, *bigq_count;  // queries with deferred cells
+    const uint32_t *big_start; // [nq + 1] packed per-query cell ranges (split scan; null: big_cap stride)
+    // record mode (query-split sharding): every visited non-empty cell is recorded as
+    // (oi * T + oj, global count, cell_base bits, 0) instead of scanned
+    int4 *record;
+    uint32_t *record_n;
+    int record_cap;
     const float *rot1, *rot2;  // HBPQ per-half rotations (optional)
     bool exact;                // reference operation order for every engine (bpq_index_desc.fbpq_exact)
     double rho;
@@ -451,30 +458,6 @@ struct LaneLut {
     }
 };
 
-// rotate the M code bytes right by L.rot bytes: byte i of the result is
-// part (rot + i) % M of the entry
-template <int MT>
-__device__ __forceinline__ void rotate_code(const uint32_t (&w)[4], int rot, uint32_t (&r)[4]) {
-    const uint32_t sh = 8u * (uint32_t)(rot & 3);
-    if constexpr (MT == 8) {
-        const bool sw = (rot & 4) != 0;
-        const uint32_t a0 = sw ? w[1] : w[0], a1 = sw ? w[0] : w[1];
-        r[0] = __funnelshift_r(a0, a1, sh);
-        r[1] = __funnelshift_r(a1, a0, sh);
-        r[2] = r[3] = 0;
-    } else {
-        const int q = rot >> 2;
-        uint32_t b0 = (q & 2) ? w[2] : w[0], b1 = (q & 2) ? w[3] : w[1];
-        uint32_t b2 = (q & 2) ? w[0] : w[2], b3 = (q & 2) ? w[1] : w[3];
-        const uint32_t a0 = (q & 1) ? b1 : b0, a1 = (q & 1) ? b2 : b1;
-        const uint32_t a2 = (q & 1) ? b3 : b2, a3 = (q & 1) ? b0 : b3;
-        r[0] = __funnelshift_r(a0, a1, sh);
-        r[1] = __funnelshift_r(a1, a2, sh);
-        r[2] = __funnelshift_r(a2, a3, sh);
-        r[3] = __funnelshift_r(a3, a0, sh);
-    }
-}
-
 // Pairwise sum of the M step values, ((v0 + v1) + (v2 + v3)) + ..., fixed
 // structure (3 or 4 dependent adds instead of M - 1)
 template <int MT>
@@ -489,12 +472,12 @@ __device__ __forceinline__ float tree_sum(float (&v)[MT]) {
 // the same sum through the plain [p][c] fold table (small cells in the
 // traversal kernel): identical operation order, so an entry scores the same
 // bits whichever kernel scans it
+// (codes_rot: the index's copy of the codes with entry e's bytes already
+// rotated by e % M, bpq_index_create; no per-entry rotation here)
 template <int MT>
 __device__ __forceinline__ float dist_pt_plain(const float *tab, int K, int y, float cbase, float pt,
-                                               const uint32_t (&w)[4]) {
+                                               const uint32_t (&r)[4]) {
     const int x = y % MT;
-    uint32_t r[4];
-    rotate_code<MT>(w, x, r);
     float v[MT];
 #pragma unroll
     for (int i = 0; i < MT; i++) {
@@ -509,10 +492,8 @@ __device__ __forceinline__ float dist_pt_plain(const float *tab, int K, int y, f
 // the parts are summed in the lane's rotated order (pairwise), then + pt +
 // cell_base.  offb[i] = byte offset of the lane's slot for step i.
 template <int MT>
-__device__ __forceinline__ float dist_pt_rep(const char *tabb, const int (&offb)[MT], int rot, float cbase, float pt,
-                                             const uint32_t (&w)[4]) {
-    uint32_t r[4];
-    rotate_code<MT>(w, rot, r);
+__device__ __forceinline__ float dist_pt_rep(const char *tabb, const int (&offb)[MT], float cbase, float pt,
+                                             const uint32_t (&r)[4]) {
     float v[MT];
 #pragma unroll
     for (int i = 0; i < MT; i++) {
@@ -764,6 +745,7 @@ struct Query {
     unsigned long long ncand;  // uniform across the CTA
     unsigned long long popped;
     uint32_t nbig_q;           // large cells deferred to big_scan_kernel (block-uniform)
+    uint32_t nrec_q;           // cells recorded (record mode, block-uniform)
 
     __device__ Query(const Args<KT, OffT> &a, Smem &s, int64_t q, const float *tab_, float *lut_,
                      const KT *s1, const KT *s2, unsigned long long *tk_)
@@ -790,6 +772,7 @@ struct Query {
         ncand = 0;
         popped = 0;
         nbig_q = 0;
+        nrec_q = 0;
     }
 
     // plain (not read-only-path) loads: extend() appends to sr/ord in-kernel
@@ -1063,6 +1046,29 @@ struct Query {
             if constexpr (ENGINE == ENGINE_TRAVERSE) {
                 continue;
             } else {
+                if constexpr (ENGINE == BPQ_ENGINE_FBPQ) {
+                    if (A.record != nullptr) {
+                        // record mode: the cell, its global count and its base, in visit order
+                        const bool has = c < n && (filt_d < 0 || digit(filt_d, list[c]) < filt_v);
+                        uint32_t tot;
+                        const uint32_t ex = block_excl_scan(S, has ? 1u : 0u, &tot);
+                        unsigned long long g = 0;
+                        if (has) {
+                            const int4 e = list[c];
+                            g = (uint32_t)e.y;
+                            const uint32_t pos = nrec_q + ex;
+                            if (pos < (uint32_t)A.record_cap)
+                                A.record[(size_t)qi * A.record_cap + pos] =
+                                    make_int4((int)((uint32_t)oi * (uint32_t)T + (uint32_t)oj), e.y, __float_as_int(cb), 0);
+                            else
+                                S.err = 1;
+                        }
+                        ncand += block_sum_u64(S, g);
+                        nrec_q += tot;
+                        __syncthreads();
+                        continue;
+                    }
+                }
                 uint32_t E;
                 uint32_t ex = block_excl_scan(S, big ? 0u : lc, &E);
                 S.cpre[threadIdx.x] = ex;
@@ -1113,7 +1119,10 @@ struct Query {
                             }
                             own[u] = lo;
                             entry[u] = S.cstart[lo] + (e - S.cpre[lo]);
-                            load_code<MT>(A.codes + (size_t)entry[u] * M, w[u], M);
+                            // point-term FBPQ at M = 8 / 16 reads the pre-rotated copy (dist_pt_plain)
+                            const uint8_t *cbase_arr = (ENGINE == BPQ_ENGINE_FBPQ && rep_fold<MT>() && A.pterm)
+                                                           ? A.codes_rot : A.codes;
+                            load_code<MT>(cbase_arr + (size_t)entry[u] * M, w[u], M);
                             if constexpr (ENGINE == BPQ_ENGINE_FBPQ)
                                 ptv[u] = A.pterm ? __ldg(A.pterm + entry[u]) : 0.f;
                         }
@@ -1911,6 +1920,7 @@ struct Query {
             ncand = 0;
             popped = 0;
             nbig_q = 0;
+            nrec_q = 0;
             if (threadIdx.x == 0) {
                 S.ntk = 0;
                 S.thr = ~0ull;
@@ -2156,6 +2166,14 @@ struct Query {
         const int k = A.k;
         const int64_t qo = A.q0 + qi;
         if (S.err == 2) return;  // re-run by the full-sort retry pass
+        if (A.record != nullptr) {  // record mode: the visited cells are the output
+            if (threadIdx.x == 0) {
+                A.record_n[qi] = S.err ? 0xFFFFFFFFu : nrec_q;
+                if (A.out_ncand) A.out_ncand[qo] = S.err ? -1 : (int64_t)ncand;
+                if (A.out_popped) A.out_popped[qo] = S.err ? -1 : (int64_t)popped;
+            }
+            return;
+        }
         if (S.err) {
             for (int x = threadIdx.x; x < k; x += NT) {
                 A.out_d[qo * k + x] = INFINITY;
@@ -2330,10 +2348,8 @@ __global__ void __launch_bounds__(BT, 2) big_scan_kernel(Args<KT, OffT> A) {
     // entries with index % 32 == l); byte offsets into the replicated table
     const char *tabb = reinterpret_cast<const char *>(tab);
     int offb[MT];
-    int rot;
     {
         const LaneLut<MT> L((int)(threadIdx.x & 31));
-        rot = L.rot;
 #pragma unroll
         for (int i = 0; i < MT; i++) offb[i] = L.off[i] * 4;
     }
@@ -2389,7 +2405,7 @@ __global__ void __launch_bounds__(BT, 2) big_scan_kernel(Args<KT, OffT> A) {
         }
         __syncthreads();
         // stream the large cells
-        const int4 *cells = A.big_cells + (size_t)qi * A.big_cap;
+        const int4 *cells = A.big_cells + (A.big_start ? (size_t)A.big_start[qi] : (size_t)qi * A.big_cap);
         const uint32_t nb = A.big_n[qi];
         uint32_t x_i = 0, c_i = 0, x_c = 0, c_c = 0;  // issue / score cursors: cell, chunk start
         if (nb) c_i = c_c = (uint32_t)__ldg(&cells[0].x) & ~31u;
@@ -2404,7 +2420,7 @@ __global__ void __launch_bounds__(BT, 2) big_scan_kernel(Args<KT, OffT> A) {
                 unsigned long long *bar = &S.mbar[slot];
                 mbar_arrive_tx(bar, n * (MT + 4));
                 if (n) {
-                    bulk_g2s(stc + (size_t)slot * kCh * MT, A.codes + (size_t)c_i * MT, n * MT, bar);
+                    bulk_g2s(stc + (size_t)slot * kCh * MT, A.codes_rot + (size_t)c_i * MT, n * MT, bar);
                     bulk_g2s(stp + (size_t)slot * kCh, A.pterm + c_i, n * 4, bar);
                 }
             }
@@ -2450,21 +2466,29 @@ __global__ void __launch_bounds__(BT, 2) big_scan_kernel(Args<KT, OffT> A) {
                 for (int u = 0; u < kPer; u++) {
                     const uint32_t e = c_c + u * BT + threadIdx.x;
                     if (e >= b1 && e < end) {
-                        load_code<MT>(A.codes + (size_t)e * MT, w[u], MT);
+                        load_code<MT>(A.codes_rot + (size_t)e * MT, w[u], MT);
                         ptv[u] = __ldg(A.pterm + e);
                     }
                 }
             }
 #pragma unroll
-            for (int u = 0; u < kPer; u++) acc[u] = dist_pt_rep<MT>(tabb, offb, rot, cb, ptv[u], w[u]);
+            for (int u = 0; u < kPer; u++) acc[u] = dist_pt_rep<MT>(tabb, offb, cb, ptv[u], w[u]);
+            // admission: the distance bits first; the id reads of all admitted entries go out
+            // together (one exposed load latency per chunk, not one per entry)
+            uint32_t dbv[kPer], idv[kPer];
+            bool ok[kPer];
 #pragma unroll
             for (int u = 0; u < kPer; u++) {
                 const uint32_t e = c_c + u * BT + threadIdx.x;
-                const uint32_t db = canon_bits(acc[u]);
-                if (e >= lst && e < end && db <= thr_hi) {
-                    const unsigned long long kk = ((unsigned long long)db << 32) | __ldg(A.ids + e);
-                    if (kk < S.thr) tk[atomicAdd(&S.ntk, 1u)] = kk;
-                }
+                dbv[u] = canon_bits(acc[u]);
+                ok[u] = e >= lst && e < end && dbv[u] <= thr_hi;
+                idv[u] = ok[u] ? __ldg(A.ids + e) : 0u;
+            }
+            const unsigned long long thr = S.thr;
+#pragma unroll
+            for (int u = 0; u < kPer; u++) {
+                const unsigned long long kk = ((unsigned long long)dbv[u] << 32) | idv[u];
+                if (ok[u] && kk < thr) tk[atomicAdd(&S.ntk, 1u)] = kk;
             }
             c_c += kCh;
             if (c_c >= end) {
@@ -2590,10 +2614,8 @@ __global__ void __launch_bounds__(NT, 2) big_stream_kernel(Args<KT, OffT> A) {
     unsigned long long *tkw = tkall + warp * kCapW;
     const char *tabb = reinterpret_cast<const char *>(tab);
     int offb[MT];
-    int rot;
     {
         const LaneLut<MT> L(lane);
-        rot = L.rot;
 #pragma unroll
         for (int i = 0; i < MT; i++) offb[i] = L.off[i] * 4;
     }
@@ -2698,7 +2720,7 @@ __global__ void __launch_bounds__(NT, 2) big_stream_kernel(Args<KT, OffT> A) {
                 fence_proxy_async();
                 mbar_arrive_tx(bar, n * (MT + 4));
                 if (n) {
-                    bulk_g2s(stc + (size_t)slot * kCh * MT, A.codes + (size_t)c0 * MT, n * MT, bar);
+                    bulk_g2s(stc + (size_t)slot * kCh * MT, A.codes_rot + (size_t)c0 * MT, n * MT, bar);
                     bulk_g2s(stp + (size_t)slot * kCh, A.pterm + c0, n * 4, bar);
                 }
             };
@@ -2736,13 +2758,13 @@ __global__ void __launch_bounds__(NT, 2) big_stream_kernel(Args<KT, OffT> A) {
                     for (int u = 0; u < kPer; u++) {
                         const uint32_t e = c0 + warp * kPerW + u * 32 + lane;
                         if (e >= b1 && e < end) {
-                            load_code<MT>(A.codes + (size_t)e * MT, w[u], MT);
+                            load_code<MT>(A.codes_rot + (size_t)e * MT, w[u], MT);
                             ptv[u] = __ldg(A.pterm + e);
                         }
                     }
                 }
 #pragma unroll
-                for (int u = 0; u < kPer; u++) acc[u] = dist_pt_rep<MT>(tabb, offb, rot, cb, ptv[u], w[u]);
+                for (int u = 0; u < kPer; u++) acc[u] = dist_pt_rep<MT>(tabb, offb, cb, ptv[u], w[u]);
                 // admission against min(own k-th key, published bound); ids only for candidates
                 const unsigned long long g = S.gthr;
                 const unsigned long long bound = wthr < g ? wthr : g;
@@ -2871,6 +2893,7 @@ void fill_args(Args<float, uint32_t> &A, const Index &ix, const float *queries, 
     A.exact = ix.exact;
     A.ids = ix.ids;
     A.codes = ix.codes;
+    A.codes_rot = ix.codes_rot;
     A.books = ix.books;
     A.fine_norms = ix.fine_norms;
     A.cross1 = ix.cross1;
@@ -2940,6 +2963,10 @@ void fill_args(Args<float, uint32_t> &A, const Index &ix, const float *queries, 
     A.ncand_q = ws.ncand_q;
     A.bigq_list = ws.bigq_list;
     A.bigq_count = ws.bigq_count;
+    A.big_start = ws.big_start;
+    A.record = ENGINE == BPQ_ENGINE_FBPQ ? ws.record : nullptr;
+    A.record_n = ws.record_n;
+    A.record_cap = ws.record_cap;
 }
 
 template <int ENGINE, int MT>

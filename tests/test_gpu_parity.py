@@ -693,3 +693,77 @@ def test_tie_plateau_every_key_ties(torch_cuda, oracle, L):
         for x in range(q.shape[0]):
             assert set(i[x, : c[x]].view(np.uint32).tolist()) == set(wi[x, : wc[x]].tolist())
         check_topk(d, i, c, wd, wi, wc, _qn(q))
+
+
+def test_query_split_sharding_equals_single(c0, torch_cuda):
+    """Query-split sharding (sharded.SplitSearcher's steps, the 3 ranks run in
+    turn on one GPU): each shard traverses one third of the queries against
+    the global counts and records the visited cells; the concatenated lists
+    (what the all-gather delivers) are streamed by every shard over its local
+    entries; the merged lists equal the single-index answer up to the §8c(ii)
+    contract (point-term sums follow the entry's position in its own shard),
+    with identical counts."""
+    import torch
+
+    from paper_1404_1831_b200 import DeviceIndex, sharded
+
+    q = c0["queries"][:120].astype(np.float32)
+    L, k = 10_000, 100
+    tables = (c0["cn1"], c0["cn2"], c0["fine_norms"], c0["cross1"], c0["cross2"])
+    full = DeviceIndex(c1=c0["c1"], c2=c0["c2"], offsets=c0["offsets"], ids=c0["ids"], codes=c0["codes"],
+                       books=c0["books"], tables=tables)
+    want = full.search(q, L, k, "fbpq").numpy()
+    parts = sharded.split_index_arrays(c0["offsets"], c0["ids"], c0["codes"], 3)
+    searchers = [sharded.SplitSearcher(DeviceIndex(c1=c0["c1"], c2=c0["c2"], offsets=s["offsets"], ids=s["ids"],
+                                                   codes=s["codes"], books=c0["books"], tables=tables,
+                                                   global_offsets=c0["offsets"],
+                                                   num_entries_global=int(c0["offsets"][-1])))
+                 for s in parts]
+    qt = torch.from_numpy(q).cuda()
+    counts, packed = [], []
+    for r, sr in enumerate(searchers):
+        lo, hi = sharded.query_slice(q.shape[0], 3, r)
+        c, v, _ = sr.traverse(qt[lo:hi], L)
+        counts.append(c)
+        packed.append(sharded.pack_visits(c, v))
+    allc = torch.cat(counts).to(torch.int64)
+    start = torch.zeros(allc.numel() + 1, dtype=torch.int64, device=allc.device)
+    torch.cumsum(allc, 0, out=start[1:])
+    allp = torch.cat(packed)
+    local = [sr.scan(qt, k, allp, start) for sr in searchers]
+    merged = sharded.merge_results([o.dists for o in local], [o.ids for o in local], [o.counts for o in local], k)
+    got = merged.numpy()
+    np.testing.assert_array_equal(got[2], want[2])
+    check_topk(got[0], got[1], got[2], want[0], want[1], want[2], _qn(q))
+
+
+def test_split_searcher_nccl_single_rank(c0):
+    """SplitSearcher end to end through an NCCL group of one (the visit
+    exchange and the final merge both run)."""
+    import os
+
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.distributed as dist
+
+    from paper_1404_1831_b200 import DeviceIndex, sharded
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29611")
+    fresh = not dist.is_initialized()
+    if fresh:
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        tables = (c0["cn1"], c0["cn2"], c0["fine_norms"], c0["cross1"], c0["cross2"])
+        dix = DeviceIndex(c1=c0["c1"], c2=c0["c2"], offsets=c0["offsets"], ids=c0["ids"], codes=c0["codes"],
+                          books=c0["books"], tables=tables)
+        q = c0["queries"][:64].astype(np.float32)
+        want = dix.search(q, 10_000, 100, "fbpq").numpy()
+        got = sharded.SplitSearcher(dix, force_collective=True).search(torch.from_numpy(q), 10_000, 100).numpy()
+        np.testing.assert_array_equal(got[2], want[2])
+        np.testing.assert_array_equal(got[1], want[1])
+        np.testing.assert_array_equal(got[0], want[0])
+    finally:
+        if fresh:
+            dist.destroy_process_group()

@@ -80,3 +80,68 @@ def test_two_rank_gloo_merge_equals_single_index(c0, tmp_path):
     got = np.load(out)
     np.testing.assert_array_equal(got["i"], c0["fbpq_L10000_k100_ids"][:12])
     np.testing.assert_array_equal(got["d"], c0["fbpq_L10000_k100_d"][:12])
+
+
+def _split_worker(rank, world, port, c0, q, L, k, out_path):
+    """Query-split sharding over gloo: rank r traverses its query slice (the
+    oracle's traversal against the global counts), the visited-cell lists
+    are exchanged with sharded.exchange_visits, every rank scans its shard's
+    entries of all queries' cells, and the packed top-k exchange + merge of
+    ShardedSearcher follows."""
+    from oracle import oracle as orc
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    t = c0["c1"].shape[0]
+    shard = sharded.split_index_arrays(c0["offsets"], c0["ids"], c0["codes"], world)[rank]
+    tables = (c0["cn1"], c0["cn2"], c0["fine_norms"], c0["cross1"], c0["cross2"])
+    cn1, cn2, fn, x1, x2 = tables
+    nq = q.shape[0]
+    lo, hi = sharded.query_slice(nq, world, rank)
+    counts, rows = [], []
+    for x in range(lo, hi):
+        *_, r1, r2 = orc.prepare_query(c0["c1"], c0["c2"], c0["books"], fn, q[x])
+        vi, vj, _, _ = orc.traverse(c0["offsets"], r1, r2, L)  # global budget
+        lin = vi.astype(np.int64) * t + vj
+        g = np.diff(c0["offsets"])[lin]
+        rows.append(np.stack([lin, g, np.zeros_like(lin), np.zeros_like(lin)], 1).astype(np.int32))
+        counts.append(lin.shape[0])
+    counts_t = torch.tensor(counts, dtype=torch.int32)
+    packed = torch.from_numpy(np.concatenate(rows) if rows else np.zeros((0, 4), np.int32))
+    allc, allp, start = sharded.exchange_visits(counts_t, packed)
+    assert allc.shape[0] == nq and int(start[-1]) == allp.shape[0]
+    d = np.full((nq, k), np.inf, np.float32)
+    ids = np.full((nq, k), 0xFFFFFFFF, np.uint32)
+    cnt = np.zeros(nq, np.int32)
+    off = shard["offsets"]
+    for x in range(nq):
+        v = allp[int(start[x]):int(start[x + 1])].numpy()
+        lin = v[:, 0].astype(np.int64)
+        q_norm, d1, d2, fold, _, _ = orc.prepare_query(c0["c1"], c0["c2"], c0["books"], fn, q[x])
+        vi, vj = (lin // t).astype(np.int32), (lin % t).astype(np.int32)
+        ci, cd = orc.scan_tables(vi, vj, off[lin], off[lin + 1], shard["ids"], shard["codes"], q_norm, d1, d2, cn1,
+                                 cn2, fold, x1, x2)
+        si, sd = orc.select_top(ci, cd, k)
+        cnt[x] = si.shape[0]
+        ids[x, : cnt[x]] = si
+        d[x, : cnt[x]] = sd
+    mine = sharded.pack_lists(torch.from_numpy(d), torch.from_numpy(ids.view(np.int32)), torch.from_numpy(cnt))
+    parts = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(parts, mine)
+    gd, gi, gc = sharded.unpack_lists(torch.cat(parts), world, nq, k)
+    md, mi, mc = sharded.merge_results_host(gd, gi, gc, k)
+    if rank == 0:
+        np.savez(out_path, d=md, i=mi, c=mc)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_gloo_query_split_equals_single_index(c0, tmp_path):
+    q = c0["queries"][:13].astype(np.float32)  # odd count: unequal query slices
+    L, k = 10_000, 100
+    out = tmp_path / "split.npz"
+    port = 31500 + (os.getpid() % 2000)
+    mp.spawn(_split_worker, args=(2, port, c0, q, L, k, str(out)), nprocs=2, join=True)
+    got = np.load(out)
+    np.testing.assert_array_equal(got["i"], c0["fbpq_L10000_k100_ids"][:13])
+    np.testing.assert_array_equal(got["d"], c0["fbpq_L10000_k100_d"][:13])
