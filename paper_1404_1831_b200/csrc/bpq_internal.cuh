@@ -39,6 +39,7 @@ constexpr int kMultiLines = 8;          // lines a warp evaluates per threshold 
 constexpr int kLutMin = BPQ_LUT_MIN;    // cells with >= this many entries are scanned via a smem LUT
 constexpr int kBandCap = 32768;         // max cells enumerated per band
 constexpr int kMaxDim = 1024;           // queries staged in shared memory
+constexpr int kStreamPad = 256;         // entries of slack after the rotated codes / point terms (masked chunk over-reads)
 
 struct Index {
     int32_t D, T, M, K, dh, ds;

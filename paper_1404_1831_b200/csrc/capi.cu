@@ -248,7 +248,8 @@ extern "C" int bpq_index_create(const bpq_index_desc *d, int copy_from_host, bpq
     ix.exact = d->fbpq_exact != 0;
     if (ix.cross1 && ix.cross2 && ix.codes && N > 0 && !d->fbpq_exact) {
         float *pt = nullptr;
-        if (cudaMalloc(&pt, N * sizeof(float)) != cudaSuccess) {
+        // kStreamPad entries of slack: the stream kernels read whole 32-aligned chunks (masked)
+        if (cudaMalloc(&pt, (N + kStreamPad) * sizeof(float)) != cudaSuccess) {
             cudaGetLastError();
             bpq_index_destroy(h);
             return fail(BPQ_ERR_CUDA, "cannot allocate the FBPQ point-term array");
@@ -271,7 +272,7 @@ extern "C" int bpq_index_create(const bpq_index_desc *d, int copy_from_host, bpq
         if (ix.M == 8 || ix.M == 16) {
             // the point-term scans read the codes pre-rotated (cells.cu rotate_codes_kernel)
             void *cr = nullptr;
-            if (cudaMalloc(&cr, std::max<size_t>(N * M, 16)) != cudaSuccess) {
+            if (cudaMalloc(&cr, (size_t)(N + kStreamPad) * M) != cudaSuccess) {
                 cudaGetLastError();
                 bpq_index_destroy(h);
                 return fail(BPQ_ERR_CUDA, "cannot allocate the rotated code array");

@@ -2833,6 +2833,341 @@ __global__ void __launch_bounds__(NT, 2) big_stream_kernel(Args<KT, OffT> A) {
     }
 }
 
+// ------------------------------------------------------------------------
+// Register-pipelined large-cell stream (`cell_flow_kernel`, the default).
+//
+// A large cell's codes and point terms are read exactly once by exactly one
+// lane, so they go from global memory straight into registers (16-/8-byte
+// and 4-byte coalesced no-allocate loads, the next chunk's loads issued
+// before the current chunk is scored) -- no shared-memory stage, no
+// mbarrier, no barrier per chunk.  Every warp walks its own interleaved
+// chunks (32 * U consecutive entries starting at a 32-entry boundary, so
+// lane l scores entries with index % 32 == l and an entry's summation order
+// is the one dist_pt_plain / dist_pt_rep use).
+//
+// Fold table: `fold[p][c]` is stored at float index c * 64 + (p + d * M) * R
+// + g for both d = 0, 1 and every replica g < R = 32 / M (256 bytes per
+// codeword).  Lane (x = l % M, g = l / M) reads step i at byte offset
+// (c << 8) + (x * R + g) * 4 + i * R * 4: the per-lane part is one constant
+// below 128 that a single PRMT merges with the code byte (byte 0 = lane
+// constant, byte 1 = code), the per-step part is an immediate -- one PRMT
+// and one LDS per lookup, 32 distinct banks per warp-wide lookup.
+//
+// Admission is a float compare against the k-th key's distance; only warps
+// holding a passing lane enter the slow path (clamp, canonical bits, id
+// load, exact (dist, id) key compare, ballot-aggregated append to the CTA's
+// shared top-k buffer).  The stream is cut into segments: a SAFE segment is
+// short enough that even if every candidate passed the buffer could not
+// overflow (used until a k-th key exists, and to redo a failed segment); an
+// OPTIMISTIC segment is sized so its expected admissions (k / seen per
+// candidate on unordered data) fill a third of the free space.  An append
+// past the buffer raises `overflow`: the segment's appends are rolled back
+// and its head is redone as a safe segment, so any input order is answered
+// exactly.  The buffer is radix-compacted to k between segments.
+constexpr int kFlowBT = 512;
+constexpr int kFlowNW = kFlowBT / 32;
+constexpr int kFlowSlack = 4096;  // free keys above roundup(k, 256)
+#ifndef BPQ_FLOW_U8
+#define BPQ_FLOW_U8 4
+#endif
+template <int MT>
+__host__ __device__ constexpr int flow_u() { return MT == 16 ? 2 : BPQ_FLOW_U8; }  // entries per lane per half chunk
+
+struct __align__(16) FlowSmem {
+    uint32_t hist_c[256];
+    unsigned long long red[kFlowNW];
+    unsigned long long tor[kFlowNW];
+    unsigned long long thr;
+    uint32_t ntk;
+    int tsel_v;
+    uint32_t tcnt;
+    unsigned long long tsel_below;
+    unsigned long long tkey;
+    uint32_t nholes;
+    uint32_t overflow;
+    uint16_t holes[kMaxK];
+    int64_t qidx;
+    int prof_ph;
+    long long prof_t;
+};
+
+__device__ __forceinline__ uint2 ldg_stream_u2(const void *p) {
+    uint2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];\n" : "=r"(v.x), "=r"(v.y) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint4 ldg_stream_u4(const void *p) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];\n"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ float ldg_stream_f(const void *p) {
+    float v;
+    asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];\n" : "=f"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ float lds_f32(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(v) : "r"(addr));
+    return v;
+}
+
+// half a chunk in registers: U entries per lane (codes + point terms)
+template <int MT>
+struct FlowHalf {
+    static constexpr int U = flow_u<MT>();
+    uint32_t w[U][MT / 4];
+    float pt[U];
+};
+// the chunk's owning cell and this lane's first entry in the chunk
+struct FlowMeta {
+    uint32_t e0, lst, cnt;
+    float cb;
+};
+
+template <int MT, typename KT, typename OffT>
+__global__ void __launch_bounds__(kFlowBT, 2) cell_flow_kernel(Args<KT, OffT> A) {
+    static_assert(MT == 8 || MT == 16, "large-cell stream needs M = 8 or 16");
+    constexpr int BT = kFlowBT;
+    constexpr int U = flow_u<MT>();
+    constexpr int kH = 32 * U;    // entries per half chunk
+    constexpr int kCh = 2 * kH;   // entries per chunk
+    constexpr int R = 32 / MT;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    FlowSmem &S = *reinterpret_cast<FlowSmem *>(smem_raw);
+    float *tab = reinterpret_cast<float *>(smem_raw + ((sizeof(FlowSmem) + 15) & ~(size_t)15));  // [K][64]
+    unsigned long long *tk = reinterpret_cast<unsigned long long *>(smem_raw + A.tk_off);
+    const int K = A.K, k = A.k;
+    const uint32_t cap = (uint32_t)A.tkcap;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // the lane's constant part of every table offset (< 128), merged under the code byte by PRMT
+    const uint32_t lane_b = (uint32_t)(((lane % MT) * R + (lane / MT) % R) * 4);
+    const char *tabb = reinterpret_cast<const char *>(tab);
+#ifdef BPQ_PHASE_PROF
+    if (threadIdx.x == 0) {
+        S.prof_ph = PH_IDLE;
+        S.prof_t = clock64();
+    }
+#endif
+    for (;;) {
+        PROF(PH_BPRO);
+        __syncthreads();  // the previous query's table / buffer readers are done
+        if (threadIdx.x == 0) {
+            const unsigned int c = atomicAdd(A.counter, 1u);
+            S.qidx = c < *A.bigq_count ? (int64_t)A.bigq_list[c] : (int64_t)-1;
+        }
+        __syncthreads();
+        const int64_t qi = S.qidx;
+        if (qi < 0) {
+            PROF(PH_IDLE);
+            return;
+        }
+        // fold table, doubled and replicated: thread -> (p fastest, c) so each quarter warp
+        // writes one 128-byte row segment
+        const float *fq = A.fold + (size_t)qi * MT * K;
+#pragma unroll 2
+        for (int x = threadIdx.x; x < MT * K; x += BT) {
+            const int p = x % MT, c = x / MT;
+            const float v = __ldg(fq + p * K + c);
+            float *d0 = tab + c * 64 + p * R;
+            if constexpr (R == 4) {
+                const float4 vv = make_float4(v, v, v, v);
+                *reinterpret_cast<float4 *>(d0) = vv;
+                *reinterpret_cast<float4 *>(d0 + MT * R) = vv;
+            } else {
+                const float2 vv = make_float2(v, v);
+                *reinterpret_cast<float2 *>(d0) = vv;
+                *reinterpret_cast<float2 *>(d0 + MT * R) = vv;
+            }
+        }
+        // the small cells' top-k seeds the buffer; holding k keys, their largest bounds admission
+        const uint32_t n0 = A.tk_n[qi];
+        unsigned long long mx = 0;
+        for (uint32_t x = threadIdx.x; x < n0; x += BT) {
+            const unsigned long long key = A.tk_part[(size_t)qi * k + x];
+            tk[x] = key;
+            mx = key > mx ? key : mx;
+        }
+        const int4 *cells = A.big_cells + (A.big_start ? (size_t)A.big_start[qi] : (size_t)qi * A.big_cap);
+        const uint32_t nb = A.big_n[qi];
+        uint32_t csum = 0;  // chunks of this query
+        for (uint32_t x = threadIdx.x; x < nb; x += BT) {
+            const int4 cl = __ldg(&cells[x]);
+            csum += ((uint32_t)cl.x + (uint32_t)cl.y - ((uint32_t)cl.x & ~31u) + kCh - 1) / kCh;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long y = __shfl_xor_sync(0xffffffffu, mx, o);
+            mx = y > mx ? y : mx;
+            csum += __shfl_xor_sync(0xffffffffu, csum, o);
+        }
+        if (lane == 0) {
+            S.red[warp] = mx;
+            S.tor[warp] = csum;
+        }
+        __syncthreads();
+        uint32_t C = 0;
+        {
+            unsigned long long m = 0;
+#pragma unroll
+            for (int w2 = 0; w2 < kFlowNW; w2++) {
+                m = S.red[w2] > m ? S.red[w2] : m;
+                C += (uint32_t)S.tor[w2];
+            }
+            if (threadIdx.x == 0) {
+                S.ntk = n0;
+                S.thr = n0 >= (uint32_t)k ? m : ~0ull;
+                S.overflow = 0;
+            }
+        }
+        __syncthreads();
+
+        // the warp's position in the cell list: cell cx covers chunks [cpre, cend)
+        uint32_t cx = 0xFFFFFFFFu, cpre = 0, cend = 0;
+        FlowMeta mn{};  // the located chunk
+        auto locate = [&](uint32_t c) {  // c < C, non-decreasing between rewinds
+            while (c >= cend) {
+                cx++;
+                const int4 cl = __ldg(&cells[cx]);
+                mn.lst = (uint32_t)cl.x;
+                mn.cnt = (uint32_t)cl.y;
+                mn.cb = __int_as_float(cl.z);
+                cpre = cend;
+                cend += (mn.lst + mn.cnt - (mn.lst & ~31u) + kCh - 1) / kCh;
+            }
+            mn.e0 = (mn.lst & ~31u) + (c - cpre) * (uint32_t)kCh + (uint32_t)lane;
+        };
+        auto fetch = [&](FlowHalf<MT> &h, uint32_t e) {
+            const uint8_t *pc = A.codes_rot + (size_t)e * MT;
+            const float *pp = A.pterm + e;
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                if constexpr (MT == 16) {
+                    const uint4 v = ldg_stream_u4(pc + (size_t)u * 32 * MT);
+                    h.w[u][0] = v.x; h.w[u][1] = v.y; h.w[u][2] = v.z; h.w[u][3] = v.w;
+                } else {
+                    const uint2 v = ldg_stream_u2(pc + (size_t)u * 32 * MT);
+                    h.w[u][0] = v.x; h.w[u][1] = v.y;
+                }
+                h.pt[u] = ldg_stream_f(pp + u * 32);
+            }
+        };
+        // score half a chunk: entries e + 32 u of cell (lst, cnt, cb)
+        auto score = [&](const FlowHalf<MT> &h, uint32_t e, uint32_t lst, uint32_t cnt, float cb,
+                         unsigned long long thr, float thrf) {
+            float acc[U];
+            bool pass[U], any = false;
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                float v[MT];
+#pragma unroll
+                for (int i = 0; i < MT; i++) {
+                    // byte 0 = lane constant, byte 1 = code byte i, bytes 2-3 = 0
+                    const uint32_t off = __byte_perm(h.w[u][i >> 2], lane_b, 0x6504u | ((uint32_t)(i & 3) << 4));
+                    v[i] = *reinterpret_cast<const float *>(tabb + (off & 0xFFFFu) + i * R * 4);
+                }
+                acc[u] = __fadd_rn(__fadd_rn(tree_sum<MT>(v), h.pt[u]), cb);
+                pass[u] = (e + u * 32 - lst) < cnt && acc[u] <= thrf;  // negative sums clamp to 0 below
+                any |= pass[u];
+            }
+            if (__any_sync(0xffffffffu, any)) {
+                const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    unsigned long long kk = 0;
+                    bool ok = pass[u];
+                    if (ok) {
+                        const float a = acc[u] < 0.f ? 0.f : acc[u];
+                        kk = ((unsigned long long)canon_bits(a) << 32) | __ldg(A.ids + e + u * 32);
+                        ok = kk < thr;
+                    }
+                    const unsigned bal = __ballot_sync(0xffffffffu, ok);
+                    if (bal) {
+                        uint32_t base = 0;
+                        if (lane == 0) base = atomicAdd(&S.ntk, (uint32_t)__popc(bal));
+                        base = __shfl_sync(0xffffffffu, base, 0);
+                        if (ok) {
+                            const uint32_t idx = base + __popc(bal & lt);
+                            if (idx < cap) tk[idx] = kk;
+                            else S.overflow = 1u;
+                        }
+                    }
+                }
+            }
+        };
+        // the warp's chunks of [sb, se): sb + warp, + kFlowNW, ...; the next chunk's halves are
+        // fetched while the current chunk's other half is scored
+        auto run_segment = [&](uint32_t sb, uint32_t se) {
+            const unsigned long long thr = S.thr;
+            const uint32_t thi = (uint32_t)(thr >> 32);
+            const float thrf = thi >= 0x7F800000u ? INFINITY : __uint_as_float(thi);
+            uint32_t c = sb + (uint32_t)warp;
+            if (c >= se) return;
+            FlowHalf<MT> ha, hb;
+            locate(c);
+            FlowMeta mc = mn;
+            fetch(ha, mc.e0);
+            fetch(hb, mc.e0 + kH);
+            for (;;) {
+                const uint32_t cn = c + kFlowNW;
+                const bool more = cn < se;
+                score(ha, mc.e0, mc.lst, mc.cnt, mc.cb, thr, thrf);
+                if (more) {
+                    locate(cn);
+                    fetch(ha, mn.e0);
+                }
+                score(hb, mc.e0 + kH, mc.lst, mc.cnt, mc.cb, thr, thrf);
+                if (!more) break;
+                fetch(hb, mn.e0 + kH);
+                mc = mn;
+                c = cn;
+            }
+        };
+
+        uint32_t pos = 0;
+        while (pos < C) {
+            PROF(PH_BSCORE);
+            const uint32_t n_start = S.ntk;  // <= k (compacted) or the seed keys
+            const uint32_t safe = (cap - n_start) / (uint32_t)kCh;
+            uint32_t len = safe;
+            if (S.thr != ~0ull) {
+                // pos chunks seen: a candidate passes with probability ~ k / seen on unordered data
+                const unsigned long long opt = (unsigned long long)pos * (cap - n_start) / (3ull * (uint32_t)k);
+                if (opt > len) len = opt > (unsigned long long)(C - pos) ? C - pos : (uint32_t)opt;
+            }
+            if (len > C - pos) len = C - pos;
+            __syncthreads();  // everyone has read ntk / thr / overflow state
+            run_segment(pos, pos + len);
+            __syncthreads();
+            if (S.overflow) {
+                // more admissions than the buffer holds: roll the segment back, redo its head safely
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    S.ntk = n_start;
+                    S.overflow = 0;
+                }
+                cx = 0xFFFFFFFFu;  // the cursor only moves forward: walk the cell list again
+                cpre = cend = 0;
+                len = min(safe, len);
+                __syncthreads();
+                run_segment(pos, pos + len);
+                __syncthreads();
+            }
+            pos += len;
+            if (pos < C) {
+                PROF(PH_BCOMPACT);
+                topk_compact<BT>(S, tk, k);
+            }
+        }
+        PROF(PH_BFIN);
+        topk_compact<BT>(S, tk, k);
+        const int64_t qo = A.q0 + qi;
+        write_topk<BT>(S, tk, k, A.ncand_q[qi], A.out_d + qo * k, A.out_ids + qo * k, A.out_count + qo);
+    }
+}
+
 // dynamic shared memory: Smem | per-query table | sorted-key prefixes | top-k buffer
 size_t tk_offset(int tab_floats, int sr_smem, size_t kt_size) {
     return (sizeof(Smem) + (size_t)tab_floats * 4 + 2 * (size_t)sr_smem * kt_size + 15) & ~(size_t)15;
@@ -3014,6 +3349,29 @@ int launch_big_one(const Index &ix, const float *queries, int64_t q0, int64_t nq
         fill_args<BPQ_ENGINE_FBPQ, MT>(A, ix, queries, q0, nq, budget, k, ws, out_dist, out_ids, out_count,
                                        nullptr, nullptr);
         if (A.big_cells == nullptr) return BPQ_OK;
+        // default: the register-pipelined stream (cell_flow_kernel); BPQ_STREAM_TMA=1 selects the
+        // TMA-ring kernels below for A/B runs
+        if (getenv("BPQ_STREAM_TMA") == nullptr) {
+            A.tkcap = ((k + 255) & ~255) + kFlowSlack;
+            A.tk_off = (int)((((sizeof(FlowSmem) + 15) & ~(size_t)15) + (size_t)64 * ix.K * 4 + 15) & ~(size_t)15);
+            const size_t smem = (size_t)A.tk_off + (size_t)A.tkcap * 8;
+            auto kfn = cell_flow_kernel<MT, float, uint32_t>;
+            static bool fattr = false;
+            if (!fattr) {
+                int dev = 0, optin = 0;
+                BPQ_CUDA_TRY(cudaGetDevice(&dev));
+                BPQ_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+                BPQ_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+                fattr = true;
+            }
+            int occ = 0;
+            BPQ_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kFlowBT, smem));
+            if (occ < 1) return fail(BPQ_ERR_UNSUPPORTED, "large-cell stream shared memory does not fit on an SM");
+            BPQ_CUDA_TRY(cudaMemsetAsync(ws.counter, 0, sizeof(unsigned int), stream));
+            kfn<<<occ * num_sms(), kFlowBT, smem, stream>>>(A);
+            BPQ_CUDA_TRY(cudaGetLastError());
+            return BPQ_OK;
+        }
         // the warp-independent variant measured slower (per-warp compactions, looser
         // admission); it stays available for A/B runs
         constexpr int BT = 512;

@@ -17,15 +17,6 @@ int launch_search_inst<BPQ_INST_ENGINE, BPQ_INST_M>(const Index &ix, const float
     return launch_one<BPQ_INST_ENGINE, BPQ_INST_M>(ix, queries, q0, nq, budget, k, ws, od, oi, oc, on, op, s);
 }
 
-#if BPQ_INST_ENGINE == 1 && BPQ_INST_M != 0  // FBPQ (the enum is not visible to the preprocessor)
-template <>
-int launch_big_inst<BPQ_INST_M>(const Index &ix, const float *queries, int64_t q0, int64_t nq, int64_t budget,
-                                int32_t k, const SearchWorkspace &ws, float *od, uint32_t *oi, int32_t *oc,
-                                cudaStream_t s) {
-    return launch_big_one<BPQ_INST_M>(ix, queries, q0, nq, budget, k, ws, od, oi, oc, s);
-}
-#endif
-
 #if BPQ_INST_ENGINE == 1 && BPQ_INST_M == 8  // FBPQ
 int search_grid_ctas(int engine, int M) {
     // upper bound over launches: the smallest dynamic footprint gives the most CTAs

@@ -10,9 +10,15 @@ det = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_o
 want = ("Duration", "DRAM Throughput", "Memory Throughput", "L1/TEX Hit Rate", "L2 Hit Rate", "Achieved Occupancy",
         "Registers Per Thread", "Compute (SM) Throughput", "Warp Cycles Per Issued Instruction", "Issue Slots Busy",
         "Dynamic Shared Memory Per Block")
+want += ("Executed Ipc Active", "No Eligible", "Eligible Warps Per Scheduler", "Shared Memory Configuration Size",
+         "Theoretical Occupancy", "Block Limit Shared Mem", "Block Limit Registers")
+cols = None
 for row in csv.reader(det.splitlines()):
-    if len(row) > 3 and row[-3] in want:
-        print(f"{row[-3]:40s} {row[-1]:>12s} {row[-2]}")
+    if "Metric Name" in row:
+        cols = (row.index("Metric Name"), row.index("Metric Unit"), row.index("Metric Value"))
+        continue
+    if cols and len(row) > cols[2] and row[cols[0]] in want:
+        print(f"{row[cols[0]]:40s} {row[cols[2]]:>12s} {row[cols[1]]}")
 mix = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(mix.splitlines()))
