@@ -13,11 +13,15 @@ for i in "${insts[@]}"; do
   e=${i%_m*}; e=${e#e}; m=${i#*_m}
   /usr/local/cuda/bin/nvcc $F -DBPQ_INST_ENGINE=$e -DBPQ_INST_M=$m -c search_inst.cu -o build_prof/search_$i.o &
 done
+# the large-cell stream kernels live in their own translation units
+for m in 8 16; do
+  /usr/local/cuda/bin/nvcc $F -DBPQ_INST_M=$m -c stream_inst.cu -o build_prof/stream_m$m.o &
+done
 wait
 objs=()
 for o in build/*.o; do
   b=$(basename $o)
-  if [ -f build_prof/$b ] && [[ " ${insts[*]/%/.o} " == *" ${b#search_} "* ]]; then objs+=(build_prof/$b); else objs+=($o); fi
+  if [ -f build_prof/$b ] && { [[ " ${insts[*]/%/.o} " == *" ${b#search_} "* ]] || [[ $b == stream_m* ]]; }; then objs+=(build_prof/$b); else objs+=($o); fi
 done
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../libbpq_b200_prof.so "${objs[@]}" -lcudart
 echo "linked: ${objs[*]}"

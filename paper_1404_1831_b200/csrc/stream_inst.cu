@@ -1,7 +1,7 @@
 // The large-cell stream kernels (point-term FBPQ) for one M, selected by
 // -DBPQ_INST_M=<8|16> (see the Makefile): their own translation units so they
 // rebuild without the fused search kernel.
-#include "search_impl.cuh"
+#include "stream_impl.cuh"
 
 #ifndef BPQ_INST_M
 #error "compile with -DBPQ_INST_M=8 or 16"

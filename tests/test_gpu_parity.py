@@ -339,6 +339,36 @@ def test_large_cells_every_engine_vs_oracle(torch_cuda, oracle, m):
             check_topk(d, i, c, wd, wi, wc, _qn(q), **_ctx(oi, q, L))
 
 
+@pytest.mark.parametrize("m,k", [(8, 100), (16, 100), (8, 1000)])
+def test_stream_adversarial_order_rolls_back(torch_cuda, oracle, m, k):
+    """One huge cell whose entries get closer to the query as their ids grow:
+    nearly every candidate beats the k-th key so far, so the large-cell
+    stream's optimistic segments overflow the top-k buffer and take the
+    roll-back + safe-segment path (cell_flow_kernel).  Answers must still
+    follow SURVEY §8c(ii)."""
+    from paper_1404_1831_b200 import DeviceIndex
+
+    rng = np.random.default_rng(500 + m + k)
+    t, dim, kk, n = 4, 32, 32, 50_000
+    c1 = (10.0 * rng.normal(size=(t, dim // 2))).astype(np.float32)
+    c2 = (10.0 * rng.normal(size=(t, dim // 2))).astype(np.float32)
+    u = rng.normal(size=dim)
+    u /= np.linalg.norm(u)
+    shrink = 3.0 * (1.0 - np.arange(n) / n)[:, None]
+    base = (np.concatenate([c1[0], c2[0]])[None, :] + shrink * u[None, :]
+            + 0.02 * rng.normal(size=(n, dim))).astype(np.float32)
+    books = (0.5 * rng.normal(size=(m, kk, dim // m))).astype(np.float32)
+    off, ids, codes = oracle.build_index(base, c1, c2, books)
+    assert np.diff(off).max() >= 40_000
+    idx = oracle.Index(c1, c2, off, ids, codes, books=books)
+    q = (np.concatenate([c1[0], c2[0]])[None, :] + 0.05 * rng.normal(size=(6, dim))).astype(np.float32)
+    dix = DeviceIndex(c1=c1, c2=c2, offsets=off, ids=ids, codes=codes, books=books, tables=idx.tables)
+    for L in (n, 20_000):
+        wd, wi, wc, _ = oracle.search_batch_numpy(idx, "fbpq", q, L, k)
+        d, i, c = dix.search(q, L, k, "fbpq").numpy()
+        check_topk(d, i, c, wd, wi, wc, _qn(q), **_ctx(idx, q, L))
+
+
 def test_empty_index_returns_nothing(torch_cuda):
     from paper_1404_1831_b200 import DeviceIndex
 
