@@ -1,18 +1,21 @@
 """Benchmark: batched bilayer-PQ search on B200 (BASELINE.json metric).
 
-Metric: queries/s at fixed L, k (plus PQ codes scanned/s and the fused
-traversal+scan kernel's HBM roofline fraction).  Default workload is
+Metric: queries/s at fixed L, k (plus PQ codes scanned/s, per-stage CUDA-event
+times and the dominant kernel's HBM roofline fraction).  Default workload is
 BASELINE.json configs[1] (single-GPU FBPQ): N=10M clipped-integer mixture
 vectors (D=128, 4,096 components), T=4,096 per half, M=8 x 256, 10,000
 queries, L=10,000, k=100.  Data is seeded synthetic (the paper's BIGANN is
-not available); codebooks are trained on the device (setup, untimed).
+not available); the c1/c2 codebooks are the reference's own training output
+(tests/golden/c1_books.npz), the other configs train on the device (untimed).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--config c1|c0|c2] [--engine fbpq|baseline|hbpq] [--L ..] [--k ..]
+                  [--config c0|c1|c2|c3|c4|c4m16] [--engine fbpq|baseline|hbpq]
+                  [--L ..] [--k ..] [--exact] [--replicas] [--no-split]
 
-N>1 (torchrun): replicas -- every rank builds the same index and searches its
-own 10k-query batch (weak scaling; c1 fits one GPU); value is
-the whole-job rate over the max-over-ranks device time.
+N>1 (torchrun): the database is sharded by point id with the global budget
+and the query-split traversal: all ranks answer
+ONE 10k-query batch ("scaling": "strong"); value is that batch over the
+max-over-ranks device time.  --replicas runs independent copies instead.
 """
 
 from __future__ import annotations

@@ -10,12 +10,18 @@
 // cells well outside the parity contract.  The work is
 // 2*T*D flop per query -- 10.5 GFLOP per 10k-query batch at config 1 --
 // under 1% of the batch time even at FFMA rate.
+#include <cstdlib>
+
 #include <cub/block/block_radix_sort.cuh>
 #include <cub/block/block_scan.cuh>
 
 #include "bpq_internal.cuh"
 
 namespace bpq {
+
+int launch_row_cut(const float *queries, int64_t nq, int32_t D, const float *dots1, const float *dots2,
+                   const float *cn1, const float *cn2, int32_t T, float *sr1, float *sr2, int32_t *ord1,
+                   int32_t *ord2, float *ru1, float *ru2, int32_t *plen, cudaStream_t stream);
 
 namespace {
 
@@ -618,6 +624,10 @@ int launch_row_topk(const float *queries, int64_t nq, int32_t D, const float *do
                     float *sr2, int32_t *ord1, int32_t *ord2, float *ru1, float *ru2, int32_t *plen,
                     cudaStream_t stream) {
     if (nq == 0) return BPQ_OK;
+    // default: the TMA-staged, sample-cut kernel (rowcut.cu); BPQ_ROW_TOPK_OLD=1 keeps the histogram
+    // kernel below for A/B runs, and rows that are not 16-byte multiples always take it
+    if ((T & 3) == 0 && getenv("BPQ_ROW_TOPK_OLD") == nullptr)
+        return launch_row_cut(queries, nq, D, dots1, dots2, cn1, cn2, T, sr1, sr2, ord1, ord2, ru1, ru2, plen, stream);
     if (T <= kSortThreads * 4)
         return launch_row_topk_t<4>(queries, nq, D, dots1, dots2, cn1, cn2, T, sr1, sr2, ord1, ord2, ru1, ru2, plen, stream);
     if (T <= kSortThreads * 8)

@@ -696,38 +696,54 @@ __global__ void __launch_bounds__(kFlowBT, 2) cell_flow_kernel(Args<KT, OffT> A)
             PROF(PH_IDLE);
             return;
         }
-        // fold table, doubled and replicated: thread -> (p fastest, c) so each quarter warp
-        // writes one 128-byte row segment
+        // every independent read of the query goes out first (one global round trip instead of four):
+        // its fold row, the seed count and first seed keys, the cell count and first cells
         const float *fq = A.fold + (size_t)qi * MT * K;
-#pragma unroll 2
-        for (int x = threadIdx.x; x < MT * K; x += BT) {
-            const int p = x % MT, c = x / MT;
-            const float v = __ldg(fq + p * K + c);
-            float *d0 = tab + c * 64 + p * R;
-            if constexpr (R == 4) {
-                const float4 vv = make_float4(v, v, v, v);
-                *reinterpret_cast<float4 *>(d0) = vv;
-                *reinterpret_cast<float4 *>(d0 + MT * R) = vv;
-            } else {
-                const float2 vv = make_float2(v, v);
-                *reinterpret_cast<float2 *>(d0) = vv;
-                *reinterpret_cast<float2 *>(d0 + MT * R) = vv;
+        constexpr int FV = MT * 256 / BT;  // fold values per thread (K <= 256)
+        float fv[FV];
+#pragma unroll
+        for (int i = 0; i < FV; i++) {
+            const int x = threadIdx.x + i * BT;  // thread -> (p fastest, c)
+            fv[i] = x < MT * K ? __ldg(fq + (x % MT) * K + x / MT) : 0.f;
+        }
+        const uint32_t n0 = A.tk_n[qi];
+        const uint32_t nb = A.big_n[qi];
+        const unsigned long long *seeds = A.tk_part + (size_t)qi * k;
+        const unsigned long long key0 = (int)threadIdx.x < k ? seeds[threadIdx.x] : 0ull;  // speculative: row is [k]
+        const bool packed = A.big_start != nullptr;
+        const int4 *cells = A.big_cells + (packed ? (size_t)A.big_start[qi] : (size_t)qi * A.big_cap);
+        int4 cl0 = make_int4(0, 0, 0, 0);
+        if (!packed && (int)threadIdx.x < A.big_cap) cl0 = __ldg(&cells[threadIdx.x]);  // speculative: row is [big_cap]
+        // fold table, doubled and replicated: each quarter warp writes one 128-byte row segment
+#pragma unroll
+        for (int i = 0; i < FV; i++) {
+            const int x = threadIdx.x + i * BT;
+            if (x < MT * K) {
+                const int p = x % MT, c = x / MT;
+                const float v = fv[i];
+                float *d0 = tab + c * 64 + p * R;
+                if constexpr (R == 4) {
+                    const float4 vv = make_float4(v, v, v, v);
+                    *reinterpret_cast<float4 *>(d0) = vv;
+                    *reinterpret_cast<float4 *>(d0 + MT * R) = vv;
+                } else {
+                    const float2 vv = make_float2(v, v);
+                    *reinterpret_cast<float2 *>(d0) = vv;
+                    *reinterpret_cast<float2 *>(d0 + MT * R) = vv;
+                }
             }
         }
         // the small cells' top-k seeds the buffer; holding k keys, their largest bounds admission
-        const uint32_t n0 = A.tk_n[qi];
         unsigned long long mx = 0;
         for (uint32_t x = threadIdx.x; x < n0; x += BT) {
-            const unsigned long long key = A.tk_part[(size_t)qi * k + x];
+            const unsigned long long key = x < (uint32_t)BT ? key0 : seeds[x];
             tk[x] = key;
             mx = key > mx ? key : mx;
         }
-        const int4 *cells = A.big_cells + (A.big_start ? (size_t)A.big_start[qi] : (size_t)qi * A.big_cap);
-        const uint32_t nb = A.big_n[qi];
         uint32_t csum = 0;  // chunks of this query
         unsigned long long esum = 0;
         for (uint32_t x = threadIdx.x; x < nb; x += BT) {
-            const int4 cl = __ldg(&cells[x]);
+            const int4 cl = (!packed && x < (uint32_t)BT) ? cl0 : __ldg(&cells[x]);
             csum += ((uint32_t)cl.x + (uint32_t)cl.y - ((uint32_t)cl.x & ~31u) + kCh - 1) / kCh;
             esum += (uint32_t)cl.y;
         }

@@ -499,6 +499,47 @@ def test_scale_sparse_index_vs_oracle(torch_cuda, oracle):
                    want_ncand=wn, **_ctx(idx, q[:48], L))
 
 
+@pytest.mark.parametrize("t,n,m,L", [(4096, 2_000_000, 8, 10_000), (16384, 4_000_000, 8, 10_000),
+                                     (16384, 2_000_000, 16, 30_000)])
+def test_config_shapes_vs_oracle(torch_cuda, oracle, t, n, m, L):
+    """BASELINE configs 1 and 4 at their table shapes (T = 4096 / 16384 per
+    half, 128-d clipped-integer mixture with T components, M = 8 / 16 x 256)
+    on a base small enough for a test: tensor-core first layer, partial row
+    sort with T / 512 keys per thread, sparse traversal, small-cell scan and
+    the large-cell stream, 64 queries against the C oracle with every
+    mismatch classified."""
+    import torch
+
+    from paper_1404_1831_b200 import datagen, encode
+
+    dev = torch.device("cuda")
+    dim, ntrain = 128, 16 * t
+    cent = datagen.mixture_centres(t, dim)
+    train = datagen.clipped_mixture_torch(ntrain, dim, t, datagen.SEED_TRAIN, dev, cent)
+    c1 = encode.train_kmeans(train[:, :64].contiguous(), t, iters=4, seed=1)
+    c2 = encode.train_kmeans(train[:, 64:].contiguous(), t, iters=4, seed=2)
+    i, j = encode.assign_cells(train, c1, c2)
+    disp = train - torch.cat([torch.from_numpy(c1).to(dev)[i], torch.from_numpy(c2).to(dev)[j]], 1)
+    ds = dim // m
+    books = np.stack([encode.train_kmeans(disp[:, p * ds:(p + 1) * ds].contiguous(), 256, iters=4, seed=10 + p)
+                      for p in range(m)])
+    base = datagen.clipped_mixture_torch(n, dim, t, datagen.SEED_BASE, dev, cent)
+    dix = encode.build_index(base, c1, c2, books)
+    del base
+    assert dix.row_ptr is not None
+    q = datagen.clipped_mixture_torch(64, dim, t, datagen.SEED_QUERIES, dev, cent).cpu().numpy()
+    off = dix.offsets.cpu().numpy().view(np.uint32).astype(np.int64)
+    idx = oracle.Index(c1, c2, off, dix.ids.cpu().numpy().view(np.uint32), dix.codes.cpu().numpy(), books=books,
+                       tables=(dix.cn1.cpu().numpy(), dix.cn2.cpu().numpy(), dix.fine_norms.cpu().numpy(),
+                               dix.cross1.cpu().numpy(), dix.cross2.cpu().numpy()))
+    for budget, k in ((L, 100), (1000, 10)):
+        res = dix.search(q, budget, k, "fbpq", ncand=True)
+        d, i_, c = res.numpy()
+        wd, wi, wc, wn = oracle.search_batch_c(idx, "fbpq", q, budget, k, threads=8)
+        check_topk(d, i_, c, wd, wi, wc, _qn(q), got_ncand=res.ncand.cpu().numpy(), want_ncand=wn,
+                   **_ctx(idx, q, budget))
+
+
 def test_export_round_trip_through_bpqi(c0, c0_index, tmp_path):
     """A device index exported to BPQI/BPQT (reference layout) and reloaded
     searches identically."""
