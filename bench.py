@@ -577,6 +577,7 @@ def main():
         torch.cuda.synchronize()
         _lib.load().bpq_debug_set_phase_buffer(None)
         stream_cand = int(ctr[18].item())
+        log(f"[diag] stream entries {stream_cand:,}, roll-backs {int(ctr[20].item())}")
     if args.phase_profile:
         from paper_1404_1831_b200 import _lib
 

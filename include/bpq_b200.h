@@ -212,7 +212,9 @@ int bpq_build_cell_lists(const uint32_t *offsets, int32_t t, uint32_t *row_ptr, 
  * idle, ...) when the library was built with -DBPQ_PHASE_PROF; returns 1 if
  * compiled in, else 0.  The buffer must hold 32 counters.  Every build adds,
  * while a buffer is set, the number of entries the large-cell stream kernel
- * scans to counter 18 (bench.py: that kernel's algorithmic bytes). */
+ * scans to counter 18 (bench.py: that kernel's algorithmic bytes); a library
+ * built with -DBPQ_CHECKED (csrc/build_checked.sh) counts the stream kernel's
+ * bound violations into counter 19. */
 int bpq_debug_set_phase_buffer(unsigned long long *dev_counters);
 
 /* First-layer stage of coarse_scan (multi_index.py:283-288): dots1[q, t] =

@@ -624,9 +624,10 @@ int launch_row_topk(const float *queries, int64_t nq, int32_t D, const float *do
                     float *sr2, int32_t *ord1, int32_t *ord2, float *ru1, float *ru2, int32_t *plen,
                     cudaStream_t stream) {
     if (nq == 0) return BPQ_OK;
-    // default: the TMA-staged, sample-cut kernel (rowcut.cu); BPQ_ROW_TOPK_OLD=1 keeps the histogram
-    // kernel below for A/B runs, and rows that are not 16-byte multiples always take it
-    if ((T & 3) == 0 && getenv("BPQ_ROW_TOPK_OLD") == nullptr)
+    // BPQ_ROW_CUT=1: the TMA-staged, sample-cut kernel (rowcut.cu).  Measured on B200 against the
+    // histogram kernel below: config 4 (T = 16384) 1.29 vs 1.40 ms, config 1 (T = 4096) 0.73 vs 0.44 ms
+    // (two persistent CTAs per SM against four one-row CTAs), so it ships as an experiment, off
+    if ((T & 3) == 0 && getenv("BPQ_ROW_CUT") != nullptr)
         return launch_row_cut(queries, nq, D, dots1, dots2, cn1, cn2, T, sr1, sr2, ord1, ord2, ru1, ru2, plen, stream);
     if (T <= kSortThreads * 4)
         return launch_row_topk_t<4>(queries, nq, D, dots1, dots2, cn1, cn2, T, sr1, sr2, ord1, ord2, ru1, ru2, plen, stream);

@@ -589,8 +589,25 @@ __global__ void __launch_bounds__(NT, 2) big_stream_kernel(Args<KT, OffT> A) {
 // the buffer raises `overflow`: the segment's appends are rolled back and
 // its head is redone as a safe segment, so any input order is answered
 // exactly.  The buffer is radix-compacted to k between segments.
+// Checked build (-DBPQ_CHECKED, csrc/build_checked.sh): every index the stream kernel forms is tested
+// against its array's bound; a violation counts into counter 19 of the diagnostics buffer
+// (bpq_debug_set_phase_buffer) instead of touching memory out of range where that is possible.
+// compute-sanitizer is closed on the build pool; tests/test_gpu_parity.py runs the small cases of
+// tools/sanitize_case.py under this build and requires the counter to stay 0.
+constexpr int PROF_CHECK_FAIL = PH_N + 2;
+#ifdef BPQ_CHECKED
+#define FLOW_CHECK(cond)                                                        \
+    do {                                                                        \
+        if (!(cond) && A.prof != nullptr) atomicAdd(A.prof + PROF_CHECK_FAIL, 1ull); \
+    } while (0)
+#else
+#define FLOW_CHECK(cond) \
+    do {                 \
+    } while (0)
+#endif
+
 constexpr int kFlowBT = 512;
-constexpr int kFlowNW = kFlowBT / 32;
+constexpr int kFlowNWMax = kFlowBT / 32;
 constexpr int kFlowSlack = 4096;  // free keys above roundup(k, 256)
 #ifndef BPQ_FLOW_AHEAD
 #define BPQ_FLOW_AHEAD 0
@@ -604,8 +621,8 @@ __host__ __device__ constexpr int flow_u() { return MT == 16 ? 2 : BPQ_FLOW_U8; 
 
 struct __align__(16) FlowSmem {
     uint32_t hist_c[256];
-    unsigned long long red[kFlowNW];
-    unsigned long long tor[kFlowNW];
+    unsigned long long red[kFlowNWMax];
+    unsigned long long tor[kFlowNWMax];
     unsigned long long thr;
     uint32_t ntk;
     int tsel_v;
@@ -614,6 +631,7 @@ struct __align__(16) FlowSmem {
     unsigned long long tkey;
     uint32_t nholes;
     uint32_t overflow;
+    uint32_t save[kFlowNWMax][3];  // per-warp cursor at the segment's start
     uint16_t holes[kMaxK];
     int64_t qidx;
     int prof_ph;
@@ -655,10 +673,12 @@ struct FlowMeta {
     float cb;
 };
 
-template <int MT, typename KT, typename OffT>
-__global__ void __launch_bounds__(kFlowBT, 2) cell_flow_kernel(Args<KT, OffT> A) {
+// BT = 512: two CTAs per SM, kFlowSlack free keys.  BT = 320 (BPQ_FLOW_CTAS=3): three CTAs per SM with a
+// 512-key slack -- more, shorter segments, a third CTA to cover the per-query serial phases.
+template <int MT, int BT, typename KT, typename OffT>
+__global__ void __launch_bounds__(BT, BT == 512 ? 2 : 3) cell_flow_kernel(Args<KT, OffT> A) {
     static_assert(MT == 8 || MT == 16, "large-cell stream needs M = 8 or 16");
-    constexpr int BT = kFlowBT;
+    constexpr int kFlowNW = BT / 32;
     constexpr int U = flow_u<MT>();
     constexpr int kH = 32 * U;    // entries per half chunk
     constexpr int kCh = 2 * kH;   // entries per chunk
@@ -699,7 +719,7 @@ __global__ void __launch_bounds__(kFlowBT, 2) cell_flow_kernel(Args<KT, OffT> A)
         // every independent read of the query goes out first (one global round trip instead of four):
         // its fold row, the seed count and first seed keys, the cell count and first cells
         const float *fq = A.fold + (size_t)qi * MT * K;
-        constexpr int FV = MT * 256 / BT;  // fold values per thread (K <= 256)
+        constexpr int FV = (MT * 256 + BT - 1) / BT;  // fold values per thread (K <= 256)
         float fv[FV];
 #pragma unroll
         for (int i = 0; i < FV; i++) {
@@ -709,7 +729,8 @@ __global__ void __launch_bounds__(kFlowBT, 2) cell_flow_kernel(Args<KT, OffT> A)
         const uint32_t n0 = A.tk_n[qi];
         const uint32_t nb = A.big_n[qi];
         const unsigned long long *seeds = A.tk_part + (size_t)qi * k;
-        const unsigned long long key0 = (int)threadIdx.x < k ? seeds[threadIdx.x] : 0ull;  // speculative: row is [k]
+        // (speculative: the row is [k]; the split scan has no seeds and passes a null tk_part with n0 = 0)
+        const unsigned long long key0 = A.tk_part != nullptr && (int)threadIdx.x < k ? seeds[threadIdx.x] : 0ull;
         const bool packed = A.big_start != nullptr;
         const int4 *cells = A.big_cells + (packed ? (size_t)A.big_start[qi] : (size_t)qi * A.big_cap);
         int4 cl0 = make_int4(0, 0, 0, 0);
@@ -722,6 +743,7 @@ __global__ void __launch_bounds__(kFlowBT, 2) cell_flow_kernel(Args<KT, OffT> A)
                 const int p = x % MT, c = x / MT;
                 const float v = fv[i];
                 float *d0 = tab + c * 64 + p * R;
+                FLOW_CHECK(c * 64 + p * R + MT * R + R <= K * 64);
                 if constexpr (R == 4) {
                     const float4 vv = make_float4(v, v, v, v);
                     *reinterpret_cast<float4 *>(d0) = vv;
@@ -781,6 +803,7 @@ __global__ void __launch_bounds__(kFlowBT, 2) cell_flow_kernel(Args<KT, OffT> A)
         auto locate = [&](uint32_t c) {  // c < C, non-decreasing between rewinds
             while (c >= cend) {
                 cx++;
+                FLOW_CHECK(cx < nb);
                 const int4 cl = __ldg(&cells[cx]);
                 mn.lst = (uint32_t)cl.x;
                 mn.cnt = (uint32_t)cl.y;
@@ -811,6 +834,7 @@ __global__ void __launch_bounds__(kFlowBT, 2) cell_flow_kernel(Args<KT, OffT> A)
         auto fetch = [&](FlowHalf<MT> &h, uint32_t e) {
             const uint8_t *pc = A.codes_rot + (size_t)e * MT;
             const float *pp = A.pterm + e;
+            FLOW_CHECK((unsigned long long)e + (U - 1) * 32 < (unsigned long long)A.n_local + kStreamPad);
 #pragma unroll
             for (int u = 0; u < U; u++) {
                 if constexpr (MT == 16) {
@@ -837,6 +861,7 @@ __global__ void __launch_bounds__(kFlowBT, 2) cell_flow_kernel(Args<KT, OffT> A)
                 for (int i = 0; i < MT; i++) {
                     // byte 0 = lane constant, byte 1 = code byte i, bytes 2-3 = 0
                     const uint32_t off = __byte_perm(h.w[u][i >> 2], lane_b, 0x6504u | ((uint32_t)(i & 3) << 4));
+                    FLOW_CHECK(off + i * R * 4 + 4 <= (uint32_t)K * 256u);
                     v[i] = *reinterpret_cast<const float *>(tabb + off + i * R * 4);
                 }
                 acc[u] = __fadd_rn(__fadd_rn(tree_sum<MT>(v), h.pt[u]), cb);
@@ -885,6 +910,7 @@ __global__ void __launch_bounds__(kFlowBT, 2) cell_flow_kernel(Args<KT, OffT> A)
             const uint32_t to = min(S.ntk, cap);
             for (uint32_t x = from + threadIdx.x; x < to; x += BT) {
                 const unsigned long long kk = tk[x];
+                FLOW_CHECK((uint32_t)kk < A.n_local);
                 tk[x] = (kk & 0xFFFFFFFF00000000ull) | __ldg(A.ids + (uint32_t)kk);
             }
             __syncthreads();
@@ -944,6 +970,7 @@ __global__ void __launch_bounds__(kFlowBT, 2) cell_flow_kernel(Args<KT, OffT> A)
                 if (threadIdx.x == 0) {
                     S.ntk = n_start;
                     S.overflow = 0;
+                    if (A.prof != nullptr) atomicAdd(A.prof + PROF_CHECK_FAIL + 1, 1ull);  // roll-backs (diagnostics)
                 }
                 cx = px = 0xFFFFFFFFu;  // the cursors only move forward: walk the cell list again
                 cpre = cend = ppre = pend = 0;
@@ -982,23 +1009,28 @@ int launch_big_one(const Index &ix, const float *queries, int64_t q0, int64_t nq
         // TMA-ring kernels below for A/B runs
         if (getenv("BPQ_STREAM_TMA") == nullptr) {
             A.flow_growth = getenv("BPQ_FLOW_GROWTH") ? atoi(getenv("BPQ_FLOW_GROWTH")) : 3;  // env: A/B experiments
-            A.tkcap = ((k + 255) & ~255) + kFlowSlack;
+            const bool three = getenv("BPQ_FLOW_CTAS") != nullptr && atoi(getenv("BPQ_FLOW_CTAS")) == 3;
+            const int bt = three ? 320 : kFlowBT;
+            A.tkcap = ((k + 255) & ~255) + (three ? 512 : kFlowSlack);
             A.tk_off = (int)((((sizeof(FlowSmem) + 15) & ~(size_t)15) + (size_t)64 * ix.K * 4 + 15) & ~(size_t)15);
             const size_t smem = (size_t)A.tk_off + (size_t)A.tkcap * 8;
-            auto kfn = cell_flow_kernel<MT, float, uint32_t>;
+            auto kfn = three ? cell_flow_kernel<MT, 320, float, uint32_t> : cell_flow_kernel<MT, kFlowBT, float, uint32_t>;
             static bool fattr = false;
             if (!fattr) {
                 int dev = 0, optin = 0;
                 BPQ_CUDA_TRY(cudaGetDevice(&dev));
                 BPQ_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-                BPQ_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+                BPQ_CUDA_TRY(cudaFuncSetAttribute(cell_flow_kernel<MT, 320, float, uint32_t>,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+                BPQ_CUDA_TRY(cudaFuncSetAttribute(cell_flow_kernel<MT, kFlowBT, float, uint32_t>,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
                 fattr = true;
             }
             int occ = 0;
-            BPQ_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kFlowBT, smem));
+            BPQ_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, bt, smem));
             if (occ < 1) return fail(BPQ_ERR_UNSUPPORTED, "large-cell stream shared memory does not fit on an SM");
             BPQ_CUDA_TRY(cudaMemsetAsync(ws.counter, 0, sizeof(unsigned int), stream));
-            kfn<<<occ * num_sms(), kFlowBT, smem, stream>>>(A);
+            kfn<<<occ * num_sms(), bt, smem, stream>>>(A);
             BPQ_CUDA_TRY(cudaGetLastError());
             return BPQ_OK;
         }

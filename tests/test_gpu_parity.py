@@ -369,6 +369,34 @@ def test_stream_adversarial_order_rolls_back(torch_cuda, oracle, m, k):
         check_topk(d, i, c, wd, wi, wc, _qn(q), **_ctx(idx, q, L))
 
 
+def test_checked_build_stream_bounds(torch_cuda):
+    """compute-sanitizer is closed on the build pool, so the stream kernel
+    has a checked build (csrc/build_checked.sh, -DBPQ_CHECKED): every index
+    it forms (table offsets, entry ranges incl. the padded over-read, cell
+    cursor, id gather) is tested against its bound and violations are
+    counted.  tools/sanitize_case.py (large cells with an unaligned end,
+    k = 300 / 1000, the adversarial roll-back case) must leave the counter
+    at 0 while the kernel demonstrably ran (stream entries > 0)."""
+    import os
+    import re
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    lib = root / "paper_1404_1831_b200" / "libbpq_b200_checked.so"
+    if not lib.exists():
+        pytest.skip("checked library not built (csrc/build_checked.sh)")
+    env = dict(os.environ, BPQ_LIB=str(lib), BPQ_CHECK_REPORT="1")
+    out = subprocess.run([sys.executable, str(root / "tools" / "sanitize_case.py")], env=env, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    m = re.search(r"check_failures=(\d+) stream_entries=(\d+)", out.stdout)
+    assert m, out.stdout[-2000:]
+    assert int(m.group(1)) == 0
+    assert int(m.group(2)) > 100_000
+
+
 def test_empty_index_returns_nothing(torch_cuda):
     from paper_1404_1831_b200 import DeviceIndex
 

@@ -4,6 +4,7 @@ dense traversal), a sparse T=1500 index that exercises the partial sort, the
 in-kernel prefix extension, the retry pass and the top-k compaction, a
 large-cell M=8 index through the TMA stream kernels (warp-mode k=100 and
 CTA-mode k=300, unaligned array end), and a tie plateau (plateau windows)."""
+import os
 import sys
 from pathlib import Path
 
@@ -12,8 +13,15 @@ import torch
 
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
-from paper_1404_1831_b200 import DeviceIndex  # noqa: E402
+from paper_1404_1831_b200 import DeviceIndex, _lib  # noqa: E402
 from oracle import oracle as orc  # noqa: E402
+
+# BPQ_CHECK_REPORT=1 (with BPQ_LIB=.../libbpq_b200_checked.so): run with the diagnostics buffer set and
+# print the checked build's bound-violation counter (slot 19) and the stream kernel's entry count (slot 18)
+REPORT = os.environ.get("BPQ_CHECK_REPORT") is not None
+if REPORT:
+    ctr = torch.zeros(32, dtype=torch.int64, device="cuda")
+    _lib.load().bpq_debug_set_phase_buffer(_lib.ptr(ctr))
 
 g = np.load(ROOT / "tests" / "golden" / "c0.npz")
 tables = (g["cn1"], g["cn2"], g["fine_norms"], g["cross1"], g["cross2"])
@@ -56,5 +64,23 @@ books = (0.01 * rng.normal(size=(8, 16, 2 * dh // 8))).astype(np.float32)
 off, ids, codes = orc.build_index(base.astype(np.float32), cb, cb, books)
 pl = DeviceIndex(c1=cb, c2=cb, offsets=off, ids=ids, codes=codes, books=books, exact=True)
 pl.search(np.zeros((2, 2 * dh), np.float32), 5000, 20, "fbpq").numpy()
+# adversarial order: one huge cell whose entries get closer to the query as ids grow (roll-back path)
+t, dim, m, kk, n = 4, 32, 8, 32, 30_000
+c1 = (10.0 * rng.normal(size=(t, dim // 2))).astype(np.float32)
+c2 = (10.0 * rng.normal(size=(t, dim // 2))).astype(np.float32)
+u = rng.normal(size=dim)
+u /= np.linalg.norm(u)
+base = (np.concatenate([c1[0], c2[0]])[None, :] + 3.0 * (1.0 - np.arange(n) / n)[:, None] * u[None, :]
+        + 0.02 * rng.normal(size=(n, dim))).astype(np.float32)
+books = (0.5 * rng.normal(size=(m, kk, dim // m))).astype(np.float32)
+off, ids, codes = orc.build_index(base, c1, c2, books)
+adv = DeviceIndex(c1=c1, c2=c2, offsets=off, ids=ids, codes=codes, books=books)
+qa = (np.concatenate([c1[0], c2[0]])[None, :] + 0.05 * rng.normal(size=(4, dim))).astype(np.float32)
+for k in (100, 1000):
+    adv.search(qa, n, k, "fbpq").numpy()
 torch.cuda.synchronize()
+if REPORT:
+    _lib.load().bpq_debug_set_phase_buffer(None)
+    c = ctr.cpu().numpy()
+    print(f"check_failures={int(c[19])} stream_entries={int(c[18])}")
 print("sanitize case done")
