@@ -947,37 +947,63 @@ __global__ void __launch_bounds__(BT, BT == 512 ? 2 : 3) cell_flow_kernel(Args<K
 
         if (threadIdx.x == 0) qnext = atomicAdd(A.counter, 1u);  // latency hidden under the stream
         uint32_t pos = 0;
+        float per_chunk = -1.f;  // appends per chunk measured on the last bounded segment (< 0: none yet)
         while (pos < C) {
             PROF(PH_BSCORE);
             const uint32_t n_start = S.ntk;  // <= k (compacted) or the seed keys
-            const uint32_t safe = (cap - n_start) / (uint32_t)kCh;
+            const uint32_t free_keys = cap - n_start;
+            const uint32_t safe = free_keys / (uint32_t)kCh;
             uint32_t len = safe;
-            if (S.thr != ~0ull) {
-                // pos chunks seen: a candidate passes with probability ~ k / seen on unordered data
-                // (a segment boundary costs a barrier pair, a compaction and a cold pipeline: few, long
-                // segments beat a tighter bound)
-                unsigned long long opt = (unsigned long long)pos * (cap - n_start) / (3ull * (uint32_t)k);
-                if (A.flow_growth > 0 && opt > (unsigned long long)A.flow_growth * pos) opt = (unsigned long long)A.flow_growth * pos;
+            const bool bounded = S.thr != ~0ull;
+            if (bounded) {
+                // Optimistic length: fill about half the free space at the append rate the last bounded
+                // segment MEASURED (the bound only tightens, but cell lists are not exchangeable: later
+                // cells can be better); before any measurement, k / seen per entry on unordered data.
+                // A segment boundary costs a barrier pair, a compaction and a cold pipeline, so segments
+                // also grow by at most flow_growth x the chunks seen.
+                unsigned long long opt;
+                if (per_chunk >= 0.f) opt = (unsigned long long)(0.5f * (float)free_keys / fmaxf(per_chunk, 1e-3f));
+                else opt = (unsigned long long)pos * free_keys / (3ull * (uint32_t)k);
+                if (A.flow_growth > 0 && pos > 0 && opt > (unsigned long long)A.flow_growth * pos)
+                    opt = (unsigned long long)A.flow_growth * pos;
                 if (opt > len) len = opt > (unsigned long long)(C - pos) ? C - pos : (uint32_t)opt;
             }
             if (len > C - pos) len = C - pos;
+            if (lane == 0) {  // the cursor at the segment's start, for a roll-back
+                S.save[warp][0] = cx;
+                S.save[warp][1] = cpre;
+                S.save[warp][2] = cend;
+            }
             __syncthreads();  // everyone has read ntk / thr / overflow state
             run_segment(pos, pos + len);
             __syncthreads();
             if (S.overflow) {
                 // more admissions than the buffer holds: roll the segment back, redo its head safely
+                const float seen_rate = (float)free_keys / (float)len;  // at least this many per chunk
                 __syncthreads();
                 if (threadIdx.x == 0) {
                     S.ntk = n_start;
                     S.overflow = 0;
                     if (A.prof != nullptr) atomicAdd(A.prof + PROF_CHECK_FAIL + 1, 1ull);  // roll-backs (diagnostics)
                 }
-                cx = px = 0xFFFFFFFFu;  // the cursors only move forward: walk the cell list again
-                cpre = cend = ppre = pend = 0;
+                cx = S.save[warp][0];
+                cpre = S.save[warp][1];
+                cend = S.save[warp][2];
+                if (cx != 0xFFFFFFFFu) {  // the cell under the cursor again
+                    const int4 cl = __ldg(&cells[cx]);
+                    mn.lst = (uint32_t)cl.x;
+                    mn.cnt = (uint32_t)cl.y;
+                    mn.cb = __int_as_float(cl.z);
+                }
+                px = 0xFFFFFFFFu;
+                ppre = pend = 0;
                 len = min(safe, len);
                 __syncthreads();
                 run_segment(pos, pos + len);
                 __syncthreads();
+                per_chunk = fmaxf(seen_rate, (float)(min(S.ntk, cap) - n_start) / (float)len);
+            } else if (bounded) {
+                per_chunk = (float)(S.ntk - n_start) / (float)len;
             }
             convert_raw(n_start);
             pos += len;

@@ -15,7 +15,12 @@ for cfg in c1 c4; do
   timeout 900 $B > $o/${tag}_${cfg}_plain.json 2> $o/${tag}_${cfg}_plain.err &&
   timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -k "$KN" -c 80 --csv --log-file $o/${tag}_${cfg}_launches.csv $B > $o/${tag}_${cfg}_launches.log 2>&1
 done
-bash tools/gpu_ab.sh ${tag}_rowcut BPQ_ROW_CUT "1" "c1 c4 c3"
+for cfg in c1 c4; do
+  B="python bench.py --config $cfg --steps 2 --warmup 3 --no-cpu-baseline --recall-queries 0"
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:cell_flow -s 3 -c 1 -o $o/${tag}_${cfg}_flow $B > $o/${tag}_${cfg}_flow_ncu.log 2>&1
+done
+BPQ_LIB=$PWD/paper_1404_1831_b200/libbpq_b200_prof.so timeout 900 python bench.py --config c4 --steps 2 --warmup 3 --no-cpu-baseline --recall-queries 0 --phase-profile > $o/${tag}_c4_prof.json 2> $o/${tag}_c4_prof.err
+BPQ_LIB=$PWD/paper_1404_1831_b200/libbpq_b200_prof.so timeout 900 python bench.py --config c1 --steps 2 --warmup 3 --no-cpu-baseline --recall-queries 0 --phase-profile > $o/${tag}_c1_prof.json 2> $o/${tag}_c1_prof.err
 for f in c1 c4; do python - <<PY
 import json
 d=json.loads(open("$o/${tag}_$f.json").read().strip().splitlines()[-1])
