@@ -490,6 +490,9 @@ def main():
     ap.add_argument("--no-split", action="store_true",
                     help="sharded: replicate the first layer and traversal on every rank instead of splitting the "
                          "queries across ranks for them")
+    ap.add_argument("--e2e-pieces", type=int, default=2,
+                    help="slices of the end-to-end host-to-host call (DeviceIndex.search_host); 1 = one "
+                         "upload, one search, one download")
     ap.add_argument("--phase-profile", action="store_true",
                     help="print per-phase cycle shares of the fused kernel (needs BPQ_LIB=...libbpq_b200_prof.so)")
     args = ap.parse_args()
@@ -651,17 +654,25 @@ def main():
     oi_h = torch.empty((nq, k), dtype=torch.int32).pin_memory()
     oc_h = torch.empty((nq,), dtype=torch.int32).pin_memory()
     q_dev = torch.empty_like(q)
+    from paper_1404_1831_b200.index import SearchResult as _SR
+
+    host_out = _SR(od_h, oi_h, oc_h)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2e_ms = 0.0
     for s in range(args.steps):
         flush.fill_((s + 7) & 0xFF)
         e0.record(stream)
-        q_dev.copy_(q_host, non_blocking=True)
-        res = (searcher.search(q_dev, L, k, engine, workspace=ws) if searcher is not None
-               else dix.search(q_dev, L, k, engine, out=out, workspace=ws))
-        od_h.copy_(res.dists, non_blocking=True)
-        oi_h.copy_(res.ids, non_blocking=True)
-        oc_h.copy_(res.counts, non_blocking=True)
+        if searcher is None and args.e2e_pieces > 1:
+            # the public host-to-host call: slices pipelined over streams (copies under kernels)
+            dix.search_host(q_host, L, k, engine, out=host_out, pieces=args.e2e_pieces)
+            res = out
+        else:
+            q_dev.copy_(q_host, non_blocking=True)
+            res = (searcher.search(q_dev, L, k, engine, workspace=ws) if searcher is not None
+                   else dix.search(q_dev, L, k, engine, out=out, workspace=ws))
+            od_h.copy_(res.dists, non_blocking=True)
+            oi_h.copy_(res.ids, non_blocking=True)
+            oc_h.copy_(res.counts, non_blocking=True)
         e1.record(stream)
         torch.cuda.synchronize()
         e2e_ms += e0.elapsed_time(e1)

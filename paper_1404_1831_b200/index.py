@@ -373,6 +373,66 @@ class DeviceIndex:
         _lib.check(rc, "bpq_search")
         return out
 
+    def search_host(self, queries, L: int, k: int, engine: str = "fbpq", *, out=None, pieces: int = 2
+                    ) -> SearchResult:
+        """Batched search from HOST queries to HOST results, pipelined: the
+        batch is cut into ``pieces`` slices, each on its own CUDA stream
+        (upload -> bpq_search -> download), so the PCIe copies of one slice
+        run under the kernels of another.  ``queries`` is a pinned CPU tensor
+        (anything else is copied into one); ``out`` an optional SearchResult
+        of pinned CPU tensors to fill.  Stream-ordered on torch's current
+        stream: the results are complete once that stream is synchronized.
+        Same answers as ``search`` (queries are independent)."""
+        import torch
+
+        if not isinstance(queries, torch.Tensor):
+            queries = torch.from_numpy(np.ascontiguousarray(np.atleast_2d(queries), np.float32))
+        if queries.is_cuda:
+            raise ValueError("search_host takes host queries; use search() for device tensors")
+        queries = queries.to(torch.float32).contiguous()
+        if not queries.is_pinned():
+            queries = queries.pin_memory()
+        nq = queries.shape[0]
+        if out is None:
+            out = SearchResult(torch.empty((nq, k), dtype=torch.float32).pin_memory(),
+                               torch.empty((nq, k), dtype=torch.int32).pin_memory(),
+                               torch.empty((nq,), dtype=torch.int32).pin_memory())
+        pieces = max(1, min(int(pieces), nq)) if nq else 1
+        cur = torch.cuda.current_stream(self.device)
+        side = self.__dict__.setdefault("_side_streams", [])
+        while len(side) < pieces:
+            side.append(torch.cuda.Stream(device=self.device))
+        bufs = self.__dict__.setdefault("_host_bufs", {})
+        start = torch.cuda.Event()
+        start.record(cur)
+        done = []
+        for i in range(pieces):
+            lo, hi = nq * i // pieces, nq * (i + 1) // pieces
+            if hi == lo:
+                continue
+            s = side[i]
+            s.wait_event(start)  # ordered after the caller's earlier work
+            with torch.cuda.stream(s):
+                key = (i, hi - lo, k)
+                b = bufs.get(key)
+                if b is None:
+                    b = bufs[key] = (torch.empty((hi - lo, self.dim), dtype=torch.float32, device=self.device),
+                                     SearchResult(torch.empty((hi - lo, k), dtype=torch.float32, device=self.device),
+                                                  torch.empty((hi - lo, k), dtype=torch.int32, device=self.device),
+                                                  torch.empty((hi - lo,), dtype=torch.int32, device=self.device)))
+                qd, od = b
+                qd.copy_(queries[lo:hi], non_blocking=True)
+                self.search(qd, L, k, engine, out=od)
+                out.dists[lo:hi].copy_(od.dists, non_blocking=True)
+                out.ids[lo:hi].copy_(od.ids, non_blocking=True)
+                out.counts[lo:hi].copy_(od.counts, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(s)
+                done.append(ev)
+        for ev in done:
+            cur.wait_event(ev)
+        return out
+
     # ------------------------------------------------------------- export
     def host_arrays(self) -> dict:
         """The index in the reference's array layout (offsets int64, ids uint32)."""

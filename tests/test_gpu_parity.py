@@ -182,6 +182,30 @@ def test_per_query_api_matches_batch(c0, c0_index):
         c0_index.search(q[None], 10, 10, "hbpq")
 
 
+def test_search_host_pipelined_equals_search(c0, c0_index, torch_cuda):
+    """DeviceIndex.search_host (host queries -> host results, slices pipelined
+    over CUDA streams) returns exactly what search() returns, for any number
+    of slices, with pinned or pageable inputs and a caller-owned output."""
+    from paper_1404_1831_b200.index import SearchResult
+
+    q = c0["queries"][:301].astype(np.float32)
+    want = c0_index.search(q, 10_000, 100, "fbpq").numpy()
+    for pieces in (1, 2, 3):
+        got = c0_index.search_host(q, 10_000, 100, "fbpq", pieces=pieces)
+        torch_cuda.cuda.synchronize()
+        np.testing.assert_array_equal(got.dists.numpy(), want[0])
+        np.testing.assert_array_equal(got.ids.numpy().view(np.uint32), want[1])
+        np.testing.assert_array_equal(got.counts.numpy(), want[2])
+    out = SearchResult(torch_cuda.empty((301, 100), dtype=torch_cuda.float32).pin_memory(),
+                       torch_cuda.empty((301, 100), dtype=torch_cuda.int32).pin_memory(),
+                       torch_cuda.empty((301,), dtype=torch_cuda.int32).pin_memory())
+    qh = torch_cuda.from_numpy(q).pin_memory()
+    for _ in range(2):  # cached slice buffers are reused
+        c0_index.search_host(qh, 10_000, 100, "fbpq", out=out, pieces=2)
+        torch_cuda.cuda.synchronize()
+        np.testing.assert_array_equal(out.ids.numpy().view(np.uint32), want[1])
+
+
 def test_search_vs_oracle_small_synthetic(torch_cuda, oracle):
     """Random small index incl. empty cells, budgets below/above N, k > candidates."""
     from paper_1404_1831_b200 import DeviceIndex
