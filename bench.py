@@ -490,9 +490,9 @@ def main():
     ap.add_argument("--no-split", action="store_true",
                     help="sharded: replicate the first layer and traversal on every rank instead of splitting the "
                          "queries across ranks for them")
-    ap.add_argument("--e2e-pieces", type=int, default=2,
+    ap.add_argument("--e2e-pieces", type=int, default=1,
                     help="slices of the end-to-end host-to-host call (DeviceIndex.search_host); 1 = one "
-                         "upload, one search, one download")
+                         "upload, one search, one download (slicing over streams measured slower)")
     ap.add_argument("--phase-profile", action="store_true",
                     help="print per-phase cycle shares of the fused kernel (needs BPQ_LIB=...libbpq_b200_prof.so)")
     args = ap.parse_args()
@@ -663,7 +663,7 @@ def main():
         flush.fill_((s + 7) & 0xFF)
         e0.record(stream)
         if searcher is None and args.e2e_pieces > 1:
-            # the public host-to-host call: slices pipelined over streams (copies under kernels)
+            # A/B: the host-to-host call sliced over streams (copies under kernels; measured slower)
             dix.search_host(q_host, L, k, engine, out=host_out, pieces=args.e2e_pieces)
             res = out
         else:

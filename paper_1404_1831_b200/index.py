@@ -373,16 +373,20 @@ class DeviceIndex:
         _lib.check(rc, "bpq_search")
         return out
 
-    def search_host(self, queries, L: int, k: int, engine: str = "fbpq", *, out=None, pieces: int = 2
+    def search_host(self, queries, L: int, k: int, engine: str = "fbpq", *, out=None, pieces: int = 1
                     ) -> SearchResult:
-        """Batched search from HOST queries to HOST results, pipelined: the
-        batch is cut into ``pieces`` slices, each on its own CUDA stream
-        (upload -> bpq_search -> download), so the PCIe copies of one slice
-        run under the kernels of another.  ``queries`` is a pinned CPU tensor
-        (anything else is copied into one); ``out`` an optional SearchResult
-        of pinned CPU tensors to fill.  Stream-ordered on torch's current
-        stream: the results are complete once that stream is synchronized.
-        Same answers as ``search`` (queries are independent)."""
+        """Batched search from HOST queries to HOST results: upload ->
+        bpq_search -> download, asynchronous on a side stream and ordered on
+        torch's current stream (the results are complete once that stream is
+        synchronized).  ``queries`` is a pinned CPU tensor (anything else is
+        copied into one); ``out`` an optional SearchResult of pinned CPU
+        tensors to fill.  ``pieces`` > 1 cuts the batch into slices on their
+        own streams so the copies of one slice run under the kernels of
+        another -- measured on the B200 at config 1 this LOSES (3.9M q/s with
+        one piece, 2.8M with two, 1.9M with three): every search kernel is a
+        persistent grid that fills the GPU, so concurrent slices time-slice
+        each other while the copies are only 0.3 ms of a 2.5 ms step.  Same
+        answers as ``search`` for any ``pieces`` (queries are independent)."""
         import torch
 
         if not isinstance(queries, torch.Tensor):
