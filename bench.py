@@ -732,6 +732,12 @@ def main():
                      "frac_incl_point_term": (dom_bytes + (4 * stream_cand if stream_dominant else pt_bytes))
                                              / (dom_ms / 1e3) / 1e9 / HBM_PEAK,
                      # both search kernels (traversal + stream) over the whole 8(d) numerator
+                     # the other search kernel when the stream dominates: the traversal kernel with the rest of
+                     # the 8(d) numerator (16 B per popped cell + the small cells' candidates)
+                     "traversal_kernel": ({"ms": trav_ms, "alg_bytes": alg_bytes - dom_bytes,
+                                           "achieved": (alg_bytes - dom_bytes) / (trav_ms / 1e3) / 1e9,
+                                           "frac": (alg_bytes - dom_bytes) / (trav_ms / 1e3) / 1e9 / HBM_PEAK}
+                                          if stream_dominant else None),
                      "search_kernels_combined": {"ms": search_ms, "alg_bytes": alg_bytes, "scan_bytes": scan_bytes,
                                                  "cell_offset_bytes": cell_bytes, "point_term_bytes": pt_bytes,
                                                  "achieved": combined, "frac": combined / HBM_PEAK}},

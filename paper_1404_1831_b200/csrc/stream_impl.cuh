@@ -632,6 +632,7 @@ struct __align__(16) FlowSmem {
     uint32_t nholes;
     uint32_t overflow;
     uint32_t save[kFlowNWMax][3];  // per-warp cursor at the segment's start
+    float per_chunk;               // appends per chunk measured on the last bounded segment (< 0: none yet)
     uint16_t holes[kMaxK];
     int64_t qidx;
     int prof_ph;
@@ -793,6 +794,7 @@ __global__ void __launch_bounds__(BT, BT == 512 ? 2 : 3) cell_flow_kernel(Args<K
                 S.ntk = n0;
                 S.thr = n0 >= (uint32_t)k ? m : ~0ull;
                 S.overflow = 0;
+                S.per_chunk = -1.f;
             }
         }
         __syncthreads();
@@ -947,7 +949,6 @@ __global__ void __launch_bounds__(BT, BT == 512 ? 2 : 3) cell_flow_kernel(Args<K
 
         if (threadIdx.x == 0) qnext = atomicAdd(A.counter, 1u);  // latency hidden under the stream
         uint32_t pos = 0;
-        float per_chunk = -1.f;  // appends per chunk measured on the last bounded segment (< 0: none yet)
         while (pos < C) {
             PROF(PH_BSCORE);
             const uint32_t n_start = S.ntk;  // <= k (compacted) or the seed keys
@@ -962,6 +963,7 @@ __global__ void __launch_bounds__(BT, BT == 512 ? 2 : 3) cell_flow_kernel(Args<K
                 // A segment boundary costs a barrier pair, a compaction and a cold pipeline, so segments
                 // also grow by at most flow_growth x the chunks seen.
                 unsigned long long opt;
+                const float per_chunk = S.per_chunk;  // (kept in shared memory: nothing extra lives across the stream loop)
                 if (per_chunk >= 0.f) opt = (unsigned long long)(0.5f * (float)free_keys / fmaxf(per_chunk, 1e-3f));
                 else opt = (unsigned long long)pos * free_keys / (3ull * (uint32_t)k);
                 if (A.flow_growth > 0 && pos > 0 && opt > (unsigned long long)A.flow_growth * pos)
@@ -1001,11 +1003,12 @@ __global__ void __launch_bounds__(BT, BT == 512 ? 2 : 3) cell_flow_kernel(Args<K
                 __syncthreads();
                 run_segment(pos, pos + len);
                 __syncthreads();
-                per_chunk = fmaxf(seen_rate, (float)(min(S.ntk, cap) - n_start) / (float)len);
+                if (threadIdx.x == 0)
+                    S.per_chunk = fmaxf(seen_rate, (float)(min(S.ntk, cap) - n_start) / (float)len);
             } else if (bounded) {
-                per_chunk = (float)(S.ntk - n_start) / (float)len;
+                if (threadIdx.x == 0) S.per_chunk = (float)(S.ntk - n_start) / (float)len;
             }
-            convert_raw(n_start);
+            convert_raw(n_start);  // (ends in a barrier: per_chunk is visible to the next segment's sizing)
             pos += len;
             if (pos < C) {
                 PROF(PH_BCOMPACT);
