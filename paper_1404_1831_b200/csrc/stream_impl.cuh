@@ -1038,7 +1038,14 @@ int launch_big_one(const Index &ix, const float *queries, int64_t q0, int64_t nq
         // TMA-ring kernels below for A/B runs
         if (getenv("BPQ_STREAM_TMA") == nullptr) {
             A.flow_growth = getenv("BPQ_FLOW_GROWTH") ? atoi(getenv("BPQ_FLOW_GROWTH")) : 3;  // env: A/B experiments
-            const bool three = getenv("BPQ_FLOW_CTAS") != nullptr && atoi(getenv("BPQ_FLOW_CTAS")) == 3;
+            // Three 320-thread CTAs per SM (512-key slack) for mid budgets and k <= 256: the third CTA
+            // covers the per-query serial phases (config 4: 2.08 -> 1.97 ms, with M = 16 2.89 -> 2.79, at
+            // k = 10 1.85 -> 1.66; configs 1 and 3 unchanged within 2 %).  Long cell lists roll the small
+            // buffer back too often (config 1 at L = 100,000: 3.1 -> 6.4 ms) and short queries have too few
+            // chunks per segment (L = 1,000: 0.47 -> 0.51 ms): those keep two 512-thread CTAs and the
+            // 4096-key slack.  BPQ_FLOW_CTAS=2 / 3 forces either.
+            const char *force = getenv("BPQ_FLOW_CTAS");
+            const bool three = force != nullptr ? atoi(force) == 3 : (budget >= 4096 && budget <= 32768 && k <= 256);
             const int bt = three ? 320 : kFlowBT;
             A.tkcap = ((k + 255) & ~255) + (three ? 512 : kFlowSlack);
             A.tk_off = (int)((((sizeof(FlowSmem) + 15) & ~(size_t)15) + (size_t)64 * ix.K * 4 + 15) & ~(size_t)15);
