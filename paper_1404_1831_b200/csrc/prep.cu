@@ -626,8 +626,12 @@ int launch_row_topk(const float *queries, int64_t nq, int32_t D, const float *do
     if (nq == 0) return BPQ_OK;
     // BPQ_ROW_CUT=1: the TMA-staged, sample-cut kernel (rowcut.cu).  Measured on B200 against the
     // histogram kernel below: config 4 (T = 16384) 1.29 vs 1.40 ms, config 1 (T = 4096) 0.73 vs 0.44 ms
-    // (two persistent CTAs per SM against four one-row CTAs), so it ships as an experiment, off
-    if ((T & 3) == 0 && getenv("BPQ_ROW_CUT") != nullptr)
+    // (two persistent CTAs per SM against four one-row CTAs), so it is off for those shapes
+    // ... except for T > 8192 (32 keys per thread), where it is the faster one and the default;
+    // BPQ_ROW_CUT=0 / 1 forces either
+    const char *rc_env = getenv("BPQ_ROW_CUT");
+    const bool row_cut = rc_env != nullptr ? atoi(rc_env) != 0 : T > kSortThreads * 16;
+    if ((T & 3) == 0 && row_cut)
         return launch_row_cut(queries, nq, D, dots1, dots2, cn1, cn2, T, sr1, sr2, ord1, ord2, ru1, ru2, plen, stream);
     if (T <= kSortThreads * 4)
         return launch_row_topk_t<4>(queries, nq, D, dots1, dots2, cn1, cn2, T, sr1, sr2, ord1, ord2, ru1, ru2, plen, stream);
