@@ -4,6 +4,8 @@
 #include <cstring>
 #include <string>
 
+#include <mutex>
+
 #include "bpq_internal.cuh"
 
 namespace bpq {
@@ -30,6 +32,31 @@ struct SearchLayout {
 };
 
 // large cells (>= lut_min entries) a query can visit: all but the cutoff cell lie inside the budget
+// Side stream for the FBPQ fold (non-blocking, one per process and device; BPQ_FOLD_INLINE=1 keeps the fold
+// on the caller's stream).  Work from concurrent searches serialises on it, ordered by per-call events.
+cudaStream_t fold_side_stream() {
+    static std::mutex mu;
+    static cudaStream_t st = nullptr;
+    static int st_dev = -1;
+    static const bool inline_fold = getenv("BPQ_FOLD_INLINE") != nullptr;
+    if (inline_fold) return nullptr;
+    int dev = -1;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    std::lock_guard<std::mutex> lock(mu);
+    if (st == nullptr) {
+        if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) {
+            cudaGetLastError();
+            st = nullptr;
+            return nullptr;
+        }
+        st_dev = dev;
+    }
+    return dev == st_dev ? st : nullptr;
+}
+
 int64_t big_cells_cap(const Index &ix, int64_t budget) {
     // the stream kernel moves codes by TMA bulk copies: 16-byte aligned code array
     if (!(ix.pterm != nullptr && ix.codes_rot != nullptr && (ix.M == 8 || ix.M == 16)) ||
@@ -409,6 +436,27 @@ int search_impl(const bpq_index *index, int engine, const float *queries, int64_
             if (rr) return rr;
             qc = ws.qrot;
         }
+        // The FBPQ fold depends on the queries only: it runs on a side stream under the first layer and
+        // the row sort (the tensor-core first layer leaves most of every SM idle), ordered by two events:
+        // after everything already queued on s (the last batch's readers of ws.fold), before the search.
+        cudaEvent_t fold_done = nullptr;
+        if (engine == BPQ_ENGINE_FBPQ) {
+            cudaStream_t fs = fold_side_stream();
+            cudaEvent_t q_ready = nullptr;
+            if (fs != nullptr && cudaEventCreateWithFlags(&q_ready, cudaEventDisableTiming) == cudaSuccess &&
+                cudaEventCreateWithFlags(&fold_done, cudaEventDisableTiming) == cudaSuccess) {
+                BPQ_CUDA_TRY(cudaEventRecord(q_ready, s));
+                BPQ_CUDA_TRY(cudaStreamWaitEvent(fs, q_ready, 0));
+                int rf = launch_fold(qc, n, ix.D, ix.M, ix.K, ix.books, ix.fine_norms, ws.fold, fs);
+                if (rf) return rf;
+                BPQ_CUDA_TRY(cudaEventRecord(fold_done, fs));
+                cudaEventDestroy(q_ready);  // (released once the recorded work completes)
+            } else {
+                cudaGetLastError();
+                if (q_ready) cudaEventDestroy(q_ready);
+                fold_done = nullptr;
+            }
+        }
         int rc = ix.cimg1 ? launch_coarse_dots_tc(qc, n, ix.D, ix.cimg1, ix.cimg2, ix.T, ws.dots1, ws.dots2, s)
                           : launch_coarse_dots(qc, n, ix.D, ix.c1, ix.c2, ix.T, ws.dots1, ws.dots2, s);
         if (rc) return rc;
@@ -431,8 +479,13 @@ int search_impl(const bpq_index *index, int engine, const float *queries, int64_
         BPQ_CUDA_TRY(cudaMemsetAsync(ws.retry_count, 0, 4, s));
         if (ws.big_cells) BPQ_CUDA_TRY(cudaMemsetAsync(ws.bigq_count, 0, 4, s));
         if (engine == BPQ_ENGINE_FBPQ) {
-            rc = launch_fold(qc, n, ix.D, ix.M, ix.K, ix.books, ix.fine_norms, ws.fold, s);
-            if (rc) return rc;
+            if (fold_done != nullptr) {
+                BPQ_CUDA_TRY(cudaStreamWaitEvent(s, fold_done, 0));
+                cudaEventDestroy(fold_done);
+            } else {
+                rc = launch_fold(qc, n, ix.D, ix.M, ix.K, ix.books, ix.fine_norms, ws.fold, s);
+                if (rc) return rc;
+            }
         }
         if (ev) BPQ_CUDA_TRY(cudaEventRecord((cudaEvent_t)stage_events[2], s));
         rc = launch_search(ix, engine, qc, q0, n, budget, k, ws, out_dist, out_ids, out_count,
