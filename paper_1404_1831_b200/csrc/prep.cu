@@ -10,6 +10,7 @@
 // cells well outside the parity contract.  The work is
 // 2*T*D flop per query -- 10.5 GFLOP per 10k-query batch at config 1 --
 // under 1% of the batch time even at FFMA rate.
+#include <algorithm>
 #include <cstdlib>
 
 #include <cub/block/block_radix_sort.cuh>
@@ -193,8 +194,11 @@ __global__ void __launch_bounds__(kSortThreads) row_sort_kernel(
     __shared__ float s_part[kSortThreads / 32];
     __shared__ float s_qn;
 
-    if (qlist != nullptr && blockIdx.x >= *qcount) return;
-    const int64_t q = qlist != nullptr ? (int64_t)qlist[blockIdx.x] : (int64_t)blockIdx.x;
+    // queue mode (the retry pass): a few hundred CTAs walk the device-side list -- a grid of nq CTAs that
+    // almost all exit at once cost 35 us per batch in launch overhead alone
+    for (unsigned int row = blockIdx.x;; row += gridDim.x) {
+    if (qlist != nullptr && row >= *qcount) return;
+    const int64_t q = qlist != nullptr ? (int64_t)qlist[row] : (int64_t)row;
     const int h = blockIdx.y;
     const int dh = D / 2;
     const float *qv = Q + q * D + h * dh;
@@ -245,6 +249,9 @@ __global__ void __launch_bounds__(kSortThreads) row_sort_kernel(
             ord[rank] = vals[s];
             pos[vals[s]] = rank;
         }
+    }
+    if (qlist == nullptr) return;
+    __syncthreads();  // the sort's shared storage is reused by the next row
     }
 }
 
@@ -564,7 +571,7 @@ int launch_row_sort_t(const float *Q, int64_t nq, int32_t D, const float *dots1,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured = true;
     }
-    dim3 grid((unsigned)nq, 2);
+    dim3 grid((unsigned)(qlist != nullptr ? std::min<int64_t>(nq, 296) : nq), 2);
     row_sort_kernel<ITEMS><<<grid, kSortThreads, smem, stream>>>(Q, D, dots1, dots2, cn1, cn2, T,
                                                                  sr1, sr2, ord1, ord2, pos1, pos2, ru1, ru2,
                                                                  qlist, qcount);
